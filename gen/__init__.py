@@ -1,0 +1,158 @@
+"""Seeded synthetic input generator (shared by the CUDA path's tests/bench and the oracle).
+
+Input generation only: no method arithmetic lives here (see ``oqr_gen.c`` header for the
+recipe and its citations: SURVEY.md s8(d), BASELINE.json configs).
+
+Matrices are column-major.  A column-major ``rows x cols`` matrix with leading dimension
+``ld`` is held in a C-contiguous numpy array of shape ``(cols, ld)`` (``arr[j, i]`` is
+element ``(i, j)``), which is also how the C ABI and the oracle take it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboqr_gen.so")
+
+REFLECT, BOTTOM, TOP, SPLIT, AORTH = 0, 1, 2, 3, 5
+UCASES = {"reflect": REFLECT, "bottom": BOTTOM, "top": TOP, "split": SPLIT, "aorth": AORTH}
+
+SEED_BASE = 0x14015171
+
+# BASELINE.json configs[0..4] (m, n, kappa_A, kappa_Z); seed_k = 0x14015171 + k.
+CONFIGS = {
+    0: dict(m=200, n=10, kappa_a=1e2, kappa_z=1e2),
+    1: dict(m=4000, n=50, kappa_a=1e4, kappa_z=1e3),
+    2: dict(m=20000, n=100, kappa_a=1e2, kappa_z=1e2),
+    3: dict(m=40000, n=200, kappa_a=1e3, kappa_z=1e2),
+    4: dict(m=10000, n=100, kappa_a=1e8, kappa_z=1e6),
+}
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oqr_gen.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        cmd = f"gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -Wall -o {_LIB_PATH} {src} -lm"
+        if os.system(cmd) != 0:
+            raise RuntimeError("failed to build gen/liboqr_gen.so: " + cmd)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.c_void_p
+        lib.oqr_gen_problem.restype = ctypes.c_int
+        lib.oqr_gen_problem.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_uint64, ctypes.c_int, P, ctypes.c_int64, P, ctypes.c_int64,
+                                        P, P, P, P, P, P, P, P, P]
+        lib.oqr_gen_normal.restype = ctypes.c_double
+        lib.oqr_gen_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
+        _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+@dataclass
+class Problem:
+    """A generated instance plus the ground-truth factors of its construction."""
+    m: int
+    n: int
+    kappa_a: float
+    kappa_z: float
+    seed: int
+    ucase: str
+    A: np.ndarray | None          # (m, lda) C-order == column-major m x m
+    Z: np.ndarray                 # (n, ldz) C-order == column-major m x n
+    Yv: np.ndarray                # (4, m): V = I - Yv^T-cols T Yv^T
+    Tv: np.ndarray                # (4, 4) column-major upper triangular (Tv[c, a] = T[a, c])
+    d: np.ndarray                 # (m,) eigenvalues of A, descending
+    s: np.ndarray                 # (n,) singular values of Z, descending
+    Yu: np.ndarray
+    Tu: np.ndarray
+    Yw: np.ndarray
+    Tw: np.ndarray
+    cols: np.ndarray              # (n,) V-columns used as left singular vectors, or -1
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def lda(self) -> int:
+        return self.A.shape[1] if self.A is not None else self.m
+
+    @property
+    def ldz(self) -> int:
+        return self.Z.shape[1]
+
+
+def problem(m: int, n: int, kappa_a: float, kappa_z: float, seed: int, ucase: str = "reflect",
+            with_A: bool = True, lda: int | None = None, ldz: int | None = None,
+            A_out: np.ndarray | None = None, Z_out: np.ndarray | None = None) -> Problem:
+    """Generate (A, Z).  ``A_out``/``Z_out`` may be preallocated (e.g. pinned) float64
+    C-contiguous arrays of shape (m, lda) / (n, ldz)."""
+    lib = _load()
+    lda = m if lda is None else lda
+    ldz = m if ldz is None else ldz
+    A = None
+    if with_A:
+        A = A_out if A_out is not None else np.empty((m, lda), dtype=np.float64)
+        assert A.shape == (m, lda) and A.dtype == np.float64 and A.flags.c_contiguous
+        lda = A.shape[1]
+    Z = Z_out if Z_out is not None else np.empty((n, ldz), dtype=np.float64)
+    assert Z.shape[0] == n and Z.dtype == np.float64 and Z.flags.c_contiguous
+    ldz = Z.shape[1]
+    if lda > m and A is not None and A_out is None:
+        A[:, m:] = 0.0
+    if ldz > m and Z_out is None:
+        Z[:, m:] = 0.0
+    Yv = np.empty((4, m)); Tv = np.empty((4, 4)); d = np.empty(m); s = np.empty(n)
+    Yu = np.zeros((4, m)); Tu = np.empty((4, 4)); Yw = np.empty((4, n)); Tw = np.empty((4, 4))
+    cols = np.empty(n, dtype=np.int64)
+    rc = lib.oqr_gen_problem(m, n, float(kappa_a), float(kappa_z), seed, UCASES[ucase],
+                             _ptr(A), lda, _ptr(Z), ldz, _ptr(Yv), _ptr(Tv), _ptr(d), _ptr(s),
+                             _ptr(Yu), _ptr(Tu), _ptr(Yw), _ptr(Tw), _ptr(cols))
+    if rc != 0:
+        raise ValueError(f"oqr_gen_problem rejected arguments (m={m}, n={n}, ucase={ucase})")
+    return Problem(m, n, kappa_a, kappa_z, seed, ucase, A, Z, Yv, Tv, d, s, Yu, Tu, Yw, Tw, cols)
+
+
+def config(k: int, ucase: str = "reflect", **kw) -> Problem:
+    c = CONFIGS[k]
+    return problem(c["m"], c["n"], c["kappa_a"], c["kappa_z"], SEED_BASE + k, ucase=ucase, **kw)
+
+
+def witness(**kw) -> Problem:
+    """Config-4 breakdown witness: same (m, n, kappa_A, kappa_Z), paper case 3 alignment
+    (PAPER.md:730-732)."""
+    return config(4, ucase="split", **kw)
+
+
+def normal(seed: int, stream: int, k: int) -> float:
+    return _load().oqr_gen_normal(seed, stream, k)
+
+
+def wy_matrix(Y: np.ndarray, T: np.ndarray) -> np.ndarray:
+    """Explicit I - Y T Y^T (rows x rows) from the generator's WY factors
+    (Y given as (4, len), T column-major (4,4)).  For small pins only."""
+    Ym = Y.T  # len x 4
+    Tm = T.T  # row-major T[a, b]
+    return np.eye(Ym.shape[0]) - Ym @ Tm @ Ym.T
+
+
+def apply_wy(Y: np.ndarray, T: np.ndarray, X: np.ndarray, transpose: bool = False) -> np.ndarray:
+    """(I - Y T Y^T) X, or its transpose applied, for X (len x k) in O(len*k)."""
+    Ym = Y.T
+    Tm = T.T
+    M = Tm.T if transpose else Tm
+    return X - Ym @ (M @ (Ym.T @ X))

@@ -1,0 +1,325 @@
+/*
+ * oqr_oracle.c -- CPU FP64 ORACLE for the oblique-QR normal-equation hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load this library.  The product path
+ * (paper_1401_5171_b200/) never imports, links or executes it; the two share no code.
+ *
+ * Plain, slow, obviously-correct FP64 implementations written from the paper:
+ *   Lowery & Langou, "Stability Analysis of QR factorization in an Oblique Inner Product"
+ *   (/root/reference/PAPER.md).  Citations are PAPER.md line numbers.
+ *
+ * Arithmetic rules: IEEE binary64, round-to-nearest, no FMA contraction
+ * (-ffp-contract=off), no -ffast-math.  Every sum runs in ascending index order
+ * as written; OpenMP only splits DISJOINT outputs across threads, so results are
+ * independent of the thread count.
+ *
+ * Storage: column-major; element (i,j) of a matrix with leading dimension ld is p[j*ld+i].
+ *
+ * Pins (tests/test_oracle_pins.py): Theorem 1, the normal equation
+ * Z^T A Z = R^T R, A = I reducing to Euclidean QR
+ * (PAPER.md:82-83), brute force with an explicit A^{1/2} on tiny inputs,
+ * exact rational arithmetic on tiny inputs, and the paper's s7 closed forms
+ * (PAPER.md:693-742).  Nothing here is "parity unpinned" except the breakdown INDEX on
+ * near-singular G.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 1 (CHOLQR) step 1-2:  B = A Z;  C = Z^T B.      */
+/* B[i,l] = sum_{j=0}^{m-1} A[i,j] Z[j,l]   (j ascending)                      */
+/* G[k,l] = sum_{i=0}^{m-1} Z[i,k] B[i,l]   (i ascending)                      */
+/* ------------------------------------------------------------------------- */
+void orc_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+              double* G, int64_t ldg) {
+  double* B = (double*)malloc(sizeof(double) * m * n);
+  double* Zt = (double*)malloc(sizeof(double) * m * n); /* row-major copy: Zt[j*n+l] = Z[j,l] */
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t j = 0; j < m; j++) Zt[j * n + l] = Z[l * ldz + j];
+  const int64_t RB = 64;
+  const int64_t nblk = (m + RB - 1) / RB;
+#pragma omp parallel for schedule(static)
+  for (int64_t ib = 0; ib < nblk; ib++) {
+    int64_t i0 = ib * RB, i1 = i0 + RB < m ? i0 + RB : m;
+    for (int64_t l = 0; l < n; l++)
+      for (int64_t i = i0; i < i1; i++) B[l * m + i] = 0.0;
+    for (int64_t j = 0; j < m; j++) {
+      const double* acol = A + j * lda;
+      const double* zrow = Zt + j * n;
+      for (int64_t l = 0; l < n; l++) {
+        const double z = zrow[l];
+        double* b = B + l * m;
+        for (int64_t i = i0; i < i1; i++) b[i] += acol[i] * z; /* B[i,l] += A[i,j]*Z[j,l] */
+      }
+    }
+  }
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      const double* zk = Z + k * ldz;
+      const double* bl = B + l * m;
+      double s = 0.0;
+      for (int64_t i = 0; i < m; i++) s += zk[i] * bl[i];
+      G[l * ldg + k] = s;
+    }
+  free(B);
+  free(Zt);
+}
+
+/* Euclidean Gram (the pre-QR step of PRE-CHOLQR done as Cholesky-QR, north_star;
+ * PAPER.md:321 with the DESIGN.md reading R2):  G[k,l] = sum_i Z[i,k] Z[i,l]. */
+void orc_gram_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* G, int64_t ldg) {
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      const double* zk = Z + k * ldz;
+      const double* zl = Z + l * ldz;
+      double s = 0.0;
+      for (int64_t i = 0; i < m; i++) s += zk[i] * zl[i];
+      G[l * ldg + k] = s;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 1 step 3, PAPER.md:182 (R = chol(C), upper, R^T R = C).           */
+/* Unblocked, reads only the upper triangle of G (readings R4, R5):  */
+/*   for j: d = G[j,j] - sum_{k<j} R[k,j]^2;  if !(d > 0) return j+1;          */
+/*          R[j,j] = sqrt(d);                                                  */
+/*          R[j,l] = (G[j,l] - sum_{k<j} R[k,j] R[k,l]) / R[j,j],  l > j.      */
+/* Strictly lower part of R is set to zero.  Returns 0 or the 1-based pivot.   */
+/* ------------------------------------------------------------------------- */
+int orc_potrf(int64_t n, const double* G, int64_t ldg, double* R, int64_t ldr) {
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) R[l * ldr + k] = 0.0;
+  for (int64_t j = 0; j < n; j++) {
+    double dot = 0.0;
+    for (int64_t k = 0; k < j; k++) dot += R[j * ldr + k] * R[j * ldr + k];
+    double d = G[j * ldg + j] - dot;
+    if (!(d > 0.0)) return (int)(j + 1);
+    double rjj = sqrt(d);
+    R[j * ldr + j] = rjj;
+    for (int64_t l = j + 1; l < n; l++) {
+      double s = 0.0;
+      for (int64_t k = 0; k < j; k++) s += R[j * ldr + k] * R[l * ldr + k];
+      R[l * ldr + j] = (G[l * ldg + j] - s) / rjj;
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 1 step 4, PAPER.md:183 (Q = Z / R), row-wise substitution as in   */
+/* the backward-error statement PAPER.md:197-198:                              */
+/*   q_ij = (z_ij - sum_{k<j} q_ik r_kj) / r_jj.                               */
+/* Q may alias Z (rows are independent; each row is read before it is written) */
+/* ------------------------------------------------------------------------- */
+void orc_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
+              double* Q, int64_t ldq) {
+#pragma omp parallel
+  {
+    double* q = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < m; i++) {
+      for (int64_t j = 0; j < n; j++) {
+        double s = 0.0;
+        for (int64_t k = 0; k < j; k++) s += q[k] * R[j * ldr + k];
+        q[j] = (Z[j * ldz + i] - s) / R[j * ldr + j];
+      }
+      for (int64_t j = 0; j < n; j++) Q[j * ldq + i] = q[j];
+    }
+    free(q);
+  }
+}
+
+/* R = R2 * R1 for upper-triangular n x n ("R = US"; normal2: R = R2 R1).
+ * R[i,j] = sum_{k=i}^{j} R2[i,k] R1[k,j], k ascending; lower part zero. */
+void orc_trmm(int64_t n, const double* R2, int64_t ld2, const double* R1, int64_t ld1, double* R, int64_t ldr) {
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) {
+      double s = 0.0;
+      if (i <= j)
+        for (int64_t k = i; k <= j; k++) s += R2[k * ld2 + i] * R1[j * ld1 + k];
+      R[j * ldr + i] = s;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* The three variants.  Q: m x n (ld m), R: n x n (ld n).                      */
+/* Status: 0 ok; k in 1..n breakdown of the first Cholesky; n+k of the second. */
+/* ------------------------------------------------------------------------- */
+
+/* Algorithm 1, CHOLQR. */
+int orc_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+               double* Q, double* R) {
+  double* G = (double*)malloc(sizeof(double) * n * n);
+  orc_gram(m, n, A, lda, Z, ldz, G, n);
+  int info = orc_potrf(n, G, n, R, n);
+  free(G);
+  if (info) return info;
+  orc_trsm(m, n, Z, ldz, R, n, Q, m);
+  return 0;
+}
+
+/* Repeated CHOLQR (north_star; reading R1): two full passes, R = R2 R1. */
+int orc_normal2(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                double* Q, double* R) {
+  double* R1 = (double*)malloc(sizeof(double) * n * n);
+  double* R2 = (double*)malloc(sizeof(double) * n * n);
+  double* Q1 = (double*)malloc(sizeof(double) * m * n);
+  int info = orc_normal(m, n, A, lda, Z, ldz, Q1, R1);
+  if (!info) {
+    int info2 = orc_normal(m, n, A, lda, Q1, m, Q, R2);
+    if (info2) info = (int)n + info2;
+    else orc_trmm(n, R2, n, R1, n, R, n);
+  }
+  free(R1); free(R2); free(Q1);
+  return info;
+}
+
+/* Algorithm 2, PRE-CHOLQR with the Euclidean pre-step done by
+ * Cholesky-QR (north_star; reading R2): [Y,S] = cholqr_I(Z);
+ * [Q,U] = CHOLQR(A,Y); R = U S. */
+int orc_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+               double* Q, double* R) {
+  double* G = (double*)malloc(sizeof(double) * n * n);
+  double* S = (double*)malloc(sizeof(double) * n * n);
+  double* U = (double*)malloc(sizeof(double) * n * n);
+  double* Y = (double*)malloc(sizeof(double) * m * n);
+  orc_gram_euclid(m, n, Z, ldz, G, n);
+  int info = orc_potrf(n, G, n, S, n);
+  if (!info) {
+    orc_trsm(m, n, Z, ldz, S, n, Y, m);
+    int info2 = orc_normal(m, n, A, lda, Y, m, Q, U);
+    if (info2) info = (int)n + info2;
+    else orc_trmm(n, U, n, S, n, R, n);
+  }
+  free(G); free(S); free(U); free(Y);
+  return info;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Checkers (double-double; TwoSum / TwoProd with an explicit fma()).          */
+/* Needed because for the stable variants the measured error is the size of   */
+/* the FP64 error of forming the check itself.            */
+/* ------------------------------------------------------------------------- */
+typedef struct { double hi, lo; } dd_t;
+
+static inline dd_t two_sum(double a, double b) {
+  double s = a + b, bb = s - a;
+  dd_t r = {s, (a - (s - bb)) + (b - bb)};
+  return r;
+}
+static inline dd_t dd_add_prod(dd_t acc, double a, double b) {
+  double p = a * b, pe = fma(a, b, -p);      /* exact product p + pe */
+  dd_t s = two_sum(acc.hi, p);
+  double lo = s.lo + acc.lo + pe;
+  dd_t r = two_sum(s.hi, lo);
+  return r;
+}
+static inline dd_t dd_add_dd_prod(dd_t acc, double a, dd_t b) {
+  /* acc + a*(b.hi + b.lo) */
+  acc = dd_add_prod(acc, a, b.hi);
+  double t = a * b.lo;
+  dd_t s = two_sum(acc.hi, t);
+  return two_sum(s.hi, s.lo + acc.lo);
+}
+
+/* E = Q^T A Q - I (n x n, ld n) accumulated in double-double, rounded at the end. */
+void orc_dd_orth(int64_t m, int64_t n, const double* A, int64_t lda, const double* Q, int64_t ldq,
+                 double* E) {
+  dd_t* AQ = (dd_t*)malloc(sizeof(dd_t) * m * n);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; i++) {
+    for (int64_t l = 0; l < n; l++) {
+      dd_t s = {0.0, 0.0};
+      for (int64_t j = 0; j < m; j++) s = dd_add_prod(s, A[j * lda + i], Q[l * ldq + j]);
+      AQ[l * m + i] = s;
+    }
+  }
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      dd_t s = {k == l ? -1.0 : 0.0, 0.0};
+      for (int64_t i = 0; i < m; i++) s = dd_add_dd_prod(s, Q[k * ldq + i], AQ[l * m + i]);
+      E[l * n + k] = s.hi + s.lo;
+    }
+  free(AQ);
+}
+
+/* G = Z^T A Z in double-double (rounded) and M = |Z|^T |A| |Z| in FP64 (for the
+ * eq.mult1-2 componentwise tolerance). */
+void orc_dd_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                 double* G, double* M) {
+  dd_t* B = (dd_t*)malloc(sizeof(dd_t) * m * n);
+  double* Babs = (double*)malloc(sizeof(double) * m * n);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; i++) {
+    for (int64_t l = 0; l < n; l++) {
+      dd_t s = {0.0, 0.0};
+      double sa = 0.0;
+      for (int64_t j = 0; j < m; j++) {
+        double a = A[j * lda + i], z = Z[l * ldz + j];
+        s = dd_add_prod(s, a, z);
+        sa += fabs(a) * fabs(z);
+      }
+      B[l * m + i] = s;
+      Babs[l * m + i] = sa;
+    }
+  }
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      dd_t s = {0.0, 0.0};
+      double sa = 0.0;
+      for (int64_t i = 0; i < m; i++) {
+        s = dd_add_dd_prod(s, Z[k * ldz + i], B[l * m + i]);
+        sa += fabs(Z[k * ldz + i]) * Babs[l * m + i];
+      }
+      G[l * n + k] = s.hi + s.lo;
+      M[l * n + k] = sa;
+    }
+  free(B);
+  free(Babs);
+}
+
+/* D = Z - Q R (double-double, rounded) and QR_abs = |Q| |R| (FP64), both m x n (ld m).
+ * Inputs for the Theorem 2 representativity checks. */
+void orc_dd_resid(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* Q, int64_t ldq,
+                  const double* R, int64_t ldr, double* D, double* QRabs) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; i++) {
+    for (int64_t j = 0; j < n; j++) {
+      dd_t s = {Z[j * ldz + i], 0.0};
+      double sa = 0.0;
+      for (int64_t k = 0; k <= j; k++) {
+        double q = Q[k * ldq + i], r = R[j * ldr + k];
+        s = dd_add_prod(s, -q, r);
+        sa += fabs(q) * fabs(r);
+      }
+      D[j * m + i] = s.hi + s.lo;
+      QRabs[j * m + i] = sa;
+    }
+  }
+}
+
+/* |G - R^T R| and |R|^T |R| over the upper triangle (Cholesky backward error,
+ * eq:normal:chol PAPER.md:195-196), double-double. Outputs n x n (ld n). */
+void orc_dd_chol_resid(int64_t n, const double* G, int64_t ldg, const double* R, int64_t ldr,
+                       double* D, double* RRabs) {
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      dd_t s = {G[l * ldg + k], 0.0};
+      double sa = 0.0;
+      int64_t kmax = k < l ? k : l;
+      for (int64_t p = 0; p <= kmax; p++) {
+        double a = R[k * ldr + p], b = R[l * ldr + p];
+        s = dd_add_prod(s, -a, b);
+        sa += fabs(a) * fabs(b);
+      }
+      D[l * n + k] = s.hi + s.lo;
+      RRabs[l * n + k] = sa;
+    }
+}

@@ -1,0 +1,77 @@
+"""Generator properties: WY closed form vs explicit reflectors,
+bitwise symmetry, spectral fidelity, determinism, case selection."""
+import numpy as np
+import pytest
+
+import gen
+
+
+def _dense(a, rows):
+    return a[:, :rows].T
+
+
+def test_wy_matches_explicit_reflectors():
+    p = gen.problem(60, 7, 1e3, 1e2, 11)
+    Y = p.Yv.T
+    H = np.eye(p.m)
+    for j in range(4):
+        v = Y[:, j:j + 1]
+        assert abs(np.linalg.norm(v) - 1.0) < 1e-14
+        H = H @ (np.eye(p.m) - 2.0 * v @ v.T)
+    V = gen.wy_matrix(p.Yv, p.Tv)
+    assert np.abs(H - V).max() < 1e-14
+
+
+def test_A_bitwise_symmetric_and_spectrum():
+    p = gen.problem(150, 9, 1e6, 1e3, 5)
+    A = _dense(p.A, p.m)
+    assert np.array_equal(A, A.T)
+    V = gen.wy_matrix(p.Yv, p.Tv)
+    assert np.abs(A - V @ np.diag(p.d) @ V.T).max() < 1e-14
+    ev = np.sort(np.linalg.eigvalsh(A))[::-1]
+    assert np.abs(ev - p.d).max() < 1e-13
+    assert p.d[0] == 1.0 and abs(p.d[-1] * 1e6 - 1.0) < 1e-12
+
+
+def test_Z_singular_values():
+    p = gen.problem(120, 12, 1e2, 1e4, 7)
+    sv = np.linalg.svd(_dense(p.Z, p.m), compute_uv=False)
+    assert np.abs(sv - p.s).max() < 1e-13
+    assert p.s[0] == 1.0 and abs(p.s[-1] * 1e4 - 1.0) < 1e-12
+
+
+def test_deterministic_and_padded_ld():
+    a = gen.problem(64, 5, 1e2, 1e2, 3)
+    b = gen.problem(64, 5, 1e2, 1e2, 3, lda=70, ldz=66)
+    assert np.array_equal(a.A, b.A[:, :64])
+    assert np.array_equal(a.Z, b.Z[:, :64])
+    c = gen.problem(64, 5, 1e2, 1e2, 4)
+    assert not np.array_equal(a.Z, c.Z)
+
+
+@pytest.mark.parametrize("ucase", ["top", "bottom", "split", "aorth"])
+def test_case_columns(ucase):
+    m, n = 40, 6
+    p = gen.problem(m, n, 1e4, 1e2, 9, ucase=ucase)
+    V = gen.wy_matrix(p.Yv, p.Tv)
+    Z = _dense(p.Z, m)
+    # left singular vectors of Z span the selected eigenvectors
+    J = p.cols
+    P = V[:, J] @ V[:, J].T
+    assert np.abs(P @ Z - Z).max() < 1e-13
+    if ucase == "top":
+        assert list(J) == list(range(n))
+    if ucase == "bottom":
+        assert list(J) == list(range(m - n, m))
+    if ucase in ("split", "aorth"):
+        assert list(J) == [0, 1, 2, m - 3, m - 2, m - 1]
+    if ucase == "aorth":
+        A = _dense(p.A, m)
+        assert np.abs(Z.T @ A @ Z - np.eye(n)).max() < 1e-12
+
+
+def test_configs_recipe():
+    p = gen.config(0)
+    assert (p.m, p.n, p.kappa_a, p.kappa_z, p.seed) == (200, 10, 1e2, 1e2, 0x14015171)
+    w = gen.witness(with_A=False)
+    assert w.m == 10000 and w.n == 100 and w.ucase == "split"

@@ -1,0 +1,61 @@
+"""Mutation check for the oracle pins: apply plausible mistakes (dropped term, wrong sign,
+wrong index, transposed operand, wrong factor order) to oracle/oqr_oracle.c one at a time,
+rebuild, and confirm that tests/test_oracle_pins.py fails for each.  Restores the source.
+
+    python tools/oracle_mutation_check.py
+"""
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "oracle", "oqr_oracle.c")
+
+MUTATIONS = {
+    "gram_transposed_A": ("b[i] += acol[i] * z;", "b[i] += A[i * lda + j] * z;"),
+    "gram_drop_last_j": ("for (int64_t j = 0; j < m; j++) {\n      const double* acol",
+                         "for (int64_t j = 0; j < m - 1; j++) {\n      const double* acol"),
+    "potrf_sign": ("double d = G[j * ldg + j] - dot;", "double d = G[j * ldg + j] + dot;"),
+    "potrf_index": ("s += R[j * ldr + k] * R[l * ldr + k];", "s += R[j * ldr + k] * R[l * ldr + k + (k+1<j)];"),
+    "trsm_index": ("s += q[k] * R[j * ldr + k];", "s += q[k] * R[k * ldr + j];"),
+    "trsm_drop_div": ("q[j] = (Z[j * ldz + i] - s) / R[j * ldr + j];", "q[j] = (Z[j * ldz + i] - s);"),
+    "trmm_order": ("s += R2[k * ld2 + i] * R1[j * ld1 + k];", "s += R1[k * ld1 + i] * R2[j * ld2 + k];"),
+    "prequr_RUS_order": ("else orc_trmm(n, U, n, S, n, R, n);", "else orc_trmm(n, S, n, U, n, R, n);"),
+    "normal2_R_order": ("else orc_trmm(n, R2, n, R1, n, R, n);", "else orc_trmm(n, R1, n, R2, n, R, n);"),
+    "normal2_Q1_not_used": ("int info2 = orc_normal(m, n, A, lda, Q1, m, Q, R2);",
+                            "int info2 = orc_normal(m, n, A, lda, Z, ldz, Q, R2);"),
+    "prequr_Y_skipped": ("int info2 = orc_normal(m, n, A, lda, Y, m, Q, U);",
+                         "int info2 = orc_normal(m, n, A, lda, Z, ldz, Q, U);"),
+    "euclid_gram_index": ("s += zk[i] * zl[i];", "s += zk[i] * zk[i];"),
+}
+
+
+def main():
+    orig = open(SRC).read()
+    backup = SRC + ".bak"
+    shutil.copy(SRC, backup)
+    survivors = []
+    try:
+        for name, (a, b) in MUTATIONS.items():
+            assert a in orig, name
+            open(SRC, "w").write(orig.replace(a, b, 1))
+            r = subprocess.run(
+                f'{sys.executable} -c "import oracle; oracle.build(force=True)" && '
+                f"{sys.executable} -m pytest tests/test_oracle_pins.py -q -x 2>&1 | tail -1",
+                shell=True, capture_output=True, text=True, cwd=ROOT)
+            line = r.stdout.strip()
+            killed = "failed" in line
+            print(f"{name:24s} {'KILLED ' if killed else 'SURVIVED'}  {line}")
+            if not killed:
+                survivors.append(name)
+    finally:
+        shutil.copy(backup, SRC)
+        os.remove(backup)
+        subprocess.run(f'{sys.executable} -c "import oracle; oracle.build(force=True)"', shell=True, cwd=ROOT)
+    print("survivors:", survivors)
+    return 1 if survivors else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
