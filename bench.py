@@ -1,0 +1,328 @@
+"""Benchmark of the oblique-QR normal-equation hot path (oqr_normal) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--variant normal]
+                    [--impl reference]
+
+One step = one oqr_normal call (all of SURVEY.md s8(a): Z packing, fused Gram K1, slot reduction
+K1r, Cholesky K2, triangular solve K3) on BASELINE.json configs[3] (m = 40000, n = 200; A is
+12.8 GB > the 126 MB L2, so no L2 flush is needed between steps).  Prints ONE JSON line (rank 0).
+
+value    = whole-job FP64 GFLOP/s with inputs resident in HBM, the paper's normalisation
+           (2 m^2 n + 2 m n^2) / T, summed over ranks (N > 1: independent
+           replicas).
+e2e      = the same metric with pinned-host A, Z copied in and Q, R copied out every step.
+roofline = the fused Gram kernel K1, timed live with CUDA events on the launching stream
+           (liboqr's timing hook): achieved = 2 m^2 n flops / mean K1 launch time against the
+           measured FP64 DMMA peak (tools/k0_probe.cu, profiles/).
+cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample: the leading r x r
+           principal block of the same A and the first r rows of Z.
+--impl reference: the oracle itself timed as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+
+FP64_DMMA_PEAK_TFLOPS = 37.2   # tools/k0_probe.cu on this pool's B200 (profiles/r01_k0_probe.txt)
+PEAK_SOURCE = "measured: K0 DMMA m8n8k4 microbenchmark, sustained, profiles/r01_k0_probe.txt"
+
+
+def flops_paper(m, n):
+    return 2.0 * m * m * n + 2.0 * m * n * n
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) while the timed region runs."""
+
+    def __init__(self, dev_index: int, period: float = 0.02):
+        self.dev_index, self.period = dev_index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.dev_index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            names = {
+                "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+                "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+                "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for k, bit in names.items():
+                            if r & bit and k != "gpu_idle":
+                                self.reasons.add(k)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # pragma: no cover
+            self.error = str(e)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+def cpu_oracle_sample(p, target_s: float = 12.0):
+    """Time the CPU oracle (as it stands) on the leading r x r principal block of the config's A
+    and the first r rows of Z, with r sized for ~target_s of work.  Returns the cpu_baseline dict."""
+    import oracle
+    m, n = p.m, p.n
+    threads = len(os.sched_getaffinity(0))
+
+    def run(r):
+        A = np.ascontiguousarray(p.A[:r, :r])
+        Z = np.ascontiguousarray(p.Z[:, :r])
+        t = time.perf_counter()
+        _, _, st = oracle.normal(A, Z, r)
+        return time.perf_counter() - t, st
+
+    r = min(m, 4096)
+    dt, _ = run(r)
+    rate = flops_paper(r, n) / dt
+    # flops(r) ~ 2 r^2 n: pick r for ~target_s, in multiples of 64, capped at m
+    r2 = int(min(m, max(r, math.sqrt(target_s * rate / (2.0 * n)))) // 64 * 64)
+    if r2 > r:
+        r = r2
+        dt, _ = run(r)
+    return {"value": flops_paper(r, n) / dt / 1e9, "unit": "GFLOP/s", "cores": threads,
+            "kind": "oracle",
+            "sample": f"oracle normal on the leading {r}x{r} principal block of the config's A and "
+                      f"first {r} rows of Z (n={n}); {dt:.1f} s; OMP threads={threads}"}, r, dt
+
+
+def reference_arm(args, cfg, rank):
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+    import oracle
+    oracle.build()
+    c = gen.CONFIGS[cfg]
+    m, n = c["m"], c["n"]
+    p = gen.config(cfg)
+    base, r, _ = cpu_oracle_sample(p, target_s=6.0)
+    A = np.ascontiguousarray(p.A[:r, :r])
+    Z = np.ascontiguousarray(p.Z[:, :r])
+    fn = oracle.VARIANTS[args.variant]
+    for _ in range(args.warmup):
+        fn(A, Z, r)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        fn(A, Z, r)
+    dt = (time.perf_counter() - t) / args.steps
+    v = flops_paper(r, n) / dt / 1e9
+    base.update(value=v)
+    line = {
+        "impl": "reference", "metric": "oblique-QR GFLOP/s (FP64)", "value": v, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"configs[{cfg}] oqr_{args.variant} m={m} n={n}; "
+                                                    f"CPU oracle on leading {r}x{r} block",
+                                        "m": m, "n": n},
+        "cpu_baseline": base,
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+_registered = []
+
+
+def pinned(shape):
+    """Page-locked float64 host tensor (numpy buffer + cudaHostRegister: no power-of-two
+    rounding of torch's pinned caching allocator for the 12.8 GB A)."""
+    import torch
+    a = np.empty(shape, dtype=np.float64)
+    rc = torch.cuda.cudart().cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+    if int(rc) != 0:
+        raise RuntimeError(f"cudaHostRegister failed ({rc})")
+    _registered.append(a)
+    t = torch.from_numpy(a)
+    assert t.is_pinned()
+    return t
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--variant", default="normal", choices=["normal", "normal2", "prequr"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("OQR_BENCH_ALLOW_SHORT"), \
+        "use --warmup >= 3"
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, args.config, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1401_5171_b200 as oqr
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = gen.CONFIGS[args.config]
+    m, n = c["m"], c["n"]
+    fl = flops_paper(m, n)
+    fl_gram = 2.0 * m * m * n
+
+    # inputs: generated once on the host straight into pinned buffers, then copied to HBM
+    A_h = pinned((m, m))
+    Z_h = pinned((n, m))
+    p = gen.config(args.config, A_out=A_h.numpy(), Z_out=Z_h.numpy())
+    A = A_h.to(dev)
+    Z = Z_h.to(dev)
+    Q = torch.empty((n, m), dtype=torch.float64, device=dev)
+    R = torch.empty((n, n), dtype=torch.float64, device=dev)
+    Q_h = pinned((n, m))
+    R_h = pinned((n, n))
+    fn = oqr.VARIANTS[args.variant]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        _, _, st = fn(A, Z, Q, R)
+        assert st == 0, f"warm-up status {st}: {oqr.status_string(st)}"
+
+    # ---- timed region: inputs resident in HBM ----
+    oqr.timing_enable(True)
+    oqr.timing_reset()
+    statuses = []
+    barrier()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            statuses.append(fn(A, Z, Q, R)[2])
+        e1.record(stream)
+        barrier()
+    ms_total = e0.elapsed_time(e1)
+    gram_ms, gram_launches, launches = oqr.timing_read()
+    oqr.timing_enable(False)
+    assert all(s == 0 for s in statuses), statuses
+    t_local = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_step = float(t_local.item()) / args.steps
+    value = world * fl / (ms_step * 1e-3) / 1e9
+
+    # ---- end to end through the public call with host buffers ----
+    h2d = A_h.numel() * 8 + Z_h.numel() * 8
+    d2h = Q_h.numel() * 8 + R_h.numel() * 8
+    barrier()
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        A.copy_(A_h, non_blocking=True)
+        Z.copy_(Z_h, non_blocking=True)
+        st = fn(A, Z, Q, R)[2]
+        Q_h.copy_(Q, non_blocking=True)
+        R_h.copy_(R, non_blocking=True)
+        assert st == 0
+    e1.record(stream)
+    barrier()
+    t_e2e = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = world * fl / (float(t_e2e.item()) * 1e-3) / 1e9
+
+    if rank == 0:
+        k1_ms = gram_ms / max(gram_launches, 1)
+        achieved = fl_gram / (k1_ms * 1e-3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+        if os.path.exists(tp):
+            try:
+                t = json.load(open(tp))
+                if t.get("m") == m and t.get("n") == n:
+                    traffic = t.get("dram_bytes_per_launch")
+            except Exception:
+                pass
+        cpu = None
+        if not args.no_cpu_baseline:
+            cpu, _, _ = cpu_oracle_sample(p)
+        peaks = measured_peaks()
+        line = {
+            "metric": "oblique-QR GFLOP/s (FP64, 1 B200) and % of FP64 roofline",
+            "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"configs[{args.config}] oqr_{args.variant}: m={m}, n={n}, "
+                                   f"kappa_A={c['kappa_a']:g}, kappa_Z={c['kappa_z']:g}",
+                       "m": m, "n": n, "variant": args.variant,
+                       "flops_per_step": fl, "flop_normalisation": "2m^2n+2mn^2 (PAPER.md:959-961)",
+                       "l2": "inputs (A = %.1f GB) larger than L2; no flush" % (8 * m * m / 1e9),
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "roofline": {"bound": "tensor", "kernel": "gram_fused (K1)", "achieved": achieved,
+                         "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,
+                         "algorithmic_flops_per_launch": fl_gram, "mean_launch_ms": k1_ms,
+                         "share_of_step": k1_ms / ms_step, "peak_source": PEAK_SOURCE,
+                         "hbm_gbs_measured": peaks.get("hbm_gbs")},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,126 @@
+/*
+ * oqr.h -- C ABI of liboqr.so, the B200 (sm_100a) oblique-QR normal-equation library.
+ *
+ * Problem (s1 "Introduction"): given A (m x m) symmetric positive definite
+ * and Z (m x n) of full column rank, m >= n, find Q (m x n) and R (n x n, upper triangular,
+ * positive diagonal) with  Z = Q R  and  Q^T A Q = I.
+ *
+ * Method: Algorithm 1 "CHOLQR" (s2):
+ *     B = A Z;  C = Z^T B;  R = chol(C);  Q = Z / R.
+ * The library fuses lines 1-2 into one kernel that streams A once and never stores B.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - FP64 (IEEE binary64, round-to-nearest), column-major.  Element (i, j) of a matrix with
+ *    leading dimension ld is p[j*ld + i].  All matrix pointers are DEVICE pointers owned by
+ *    the caller; the library never frees or retains them.
+ *  - A is read in full as given (both triangles); it is never written.  Z is never written.
+ *  - lda, ldz >= m and EVEN; A and Z 16-byte aligned (the kernels move A columns with
+ *    cp.async.bulk, which needs 16-byte aligned sources).
+ *  - 1 <= n <= min(m, OQR_NMAX).
+ *  - Q: m x n output with leading dimension m.  R: n x n output with leading dimension n,
+ *    upper triangular with positive diagonal; its strictly lower part is written as zero.
+ *  - Outputs must not overlap the inputs or each other.
+ *  - All work is enqueued on `stream` (0 = legacy default stream).  Scratch memory is
+ *    stream-ordered (cudaMallocAsync / cudaFreeAsync) inside the call, so concurrent calls
+ *    on different streams are safe.
+ *
+ * Status codes (LAPACK conventions):
+ *     0        success
+ *     1..n     Cholesky breakdown at pivot k (1-based) of the FIRST Cholesky: oqr_normal,
+ *              pass 1 of oqr_normal2, the Euclidean pre-step of oqr_prequr.  A pivot
+ *              breaks down when it is <= 0 or NaN (reading R4).
+ *     n+1..2n  breakdown at pivot k of the SECOND Cholesky (pass 2 of oqr_normal2, the
+ *              A-stage of oqr_prequr); the code is n + k (LAPACK xSYGV's INFO = N + i idiom).
+ *    -i        argument i is invalid: -1 m, -2 n, -3 A (null or misaligned), -4 lda (< m or
+ *              odd), -5 Z, -6 ldz, -7 Q, -8 R.  Nothing is launched.
+ *   -100       a CUDA error occurred (launch or runtime); -101 workspace allocation failed.
+ *  On any nonzero status the contents of Q and R are unspecified.
+ *
+ * Preconditions that are NOT checked (reading R17): that A is SPD and
+ * that Z has full rank.  A violation surfaces as a breakdown status or as a large
+ * ||Q^T A Q - I||, exactly as in the CPU oracle.
+ */
+#ifndef OQR_H
+#define OQR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OQR_NMAX 240
+
+/* cudaStream_t without pulling in the CUDA headers. */
+typedef struct CUstream_st* oqr_stream_t;
+
+/*
+ * oqr_normal -- CHOLQR, Algorithm 1.
+ *   G = Z^T (A Z) (lines 1-2, fused; A streamed once), R = chol(G) (line 3),
+ *   Q = Z R^{-1} by row-wise substitution (line 4).
+ * Synchronous: enqueues on `stream`, then synchronises `stream` and returns the status.
+ */
+int oqr_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+               double* Q, double* R, oqr_stream_t stream);
+
+/*
+ * oqr_normal2 -- repeated CHOLQR (north_star; reading R1, the CGS2 analogue of
+ * PAPER.md:673-681):  [Q1, R1] = CHOLQR(A, Z);  [Q, R2] = CHOLQR(A, Q1);  R = R2 R1.
+ * The second pass re-streams A (it must see A * dQ1).  Q1 lives in Q.
+ */
+int oqr_normal2(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                double* Q, double* R, oqr_stream_t stream);
+
+/*
+ * oqr_prequr -- PRE-CHOLQR, Algorithm 2 with the Euclidean pre-QR done by
+ * Cholesky-QR as north_star specifies (reading R2):
+ *   S = chol(Z^T Z), Y = Z S^{-1};  [Q, U] = CHOLQR(A, Y);  R = U S.
+ * Y lives in Q and is overwritten in place by Q = Y U^{-1}.
+ */
+int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+               double* Q, double* R, oqr_stream_t stream);
+
+/* Human-readable text for a status code (static storage; never NULL). */
+const char* oqr_status_string(int status);
+
+/* ---- Step exports (test and measurement only).  ASYNCHRONOUS: they enqueue and return 0
+ *      (or a negative argument / CUDA status) without synchronising.  Workspace is
+ *      stream-ordered, so the caller may free nothing until the stream has drained. ---- */
+
+/* G = Z^T (A Z), Algorithm 1 lines 1-2.  G: n x n, ld n, both triangles
+ * written (G is not forced symmetric: G[k,l] = sum_i Z[i,k] (AZ)[i,l]).  Summation order is
+ * fixed for a given (m, n, SM count), so repeated calls are bitwise identical. */
+int oqr_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+             double* G, oqr_stream_t stream);
+
+/* G = Z^T Z, the Euclidean Gram of the PRE-CHOLQR pre-step (reading R2). */
+int oqr_gram_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* G,
+                    oqr_stream_t stream);
+
+/* R = chol(G), upper, R^T R = G, reading only the upper triangle of G (n x n, ld n);
+ * Algorithm 1 line 3.  *d_info (device int) receives 0 or the 1-based pivot
+ * of breakdown (pivot <= 0 or NaN).  R: n x n, ld n, strictly lower part zero. */
+int oqr_potrf(int64_t n, const double* G, double* R, int* d_info, oqr_stream_t stream);
+
+/* Q = Z R^{-1} by row-wise substitution, Algorithm 1 line 4:
+ * q_ij = (z_ij - sum_{k<j} q_ik r_kj) / r_jj.  R: n x n, ld n, upper.  Q: m x n, ld m.
+ * Q may equal Z when ldz == m (in-place). */
+int oqr_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, double* Q,
+             oqr_stream_t stream);
+
+/* ---- Measurement hook: per-launch CUDA-event timing of the fused Gram kernel (K1).
+ *      When enabled, every K1 launch is bracketed by events recorded on the caller's stream;
+ *      oqr_timing_read returns the accumulated milliseconds and launch count since the last
+ *      reset (it synchronises on the recorded events).  Not thread-safe; off by default. */
+void oqr_timing_enable(int enable);
+void oqr_timing_reset(void);
+int oqr_timing_read(double* gram_ms, int64_t* gram_launches, int64_t* total_launches);
+
+/* Number of kernels this library has launched since load (all entry points). */
+int64_t oqr_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OQR_H */

@@ -1,0 +1,212 @@
+"""Thin Python binding of liboqr.so (B200 / sm_100a oblique QR, normal-equation path).
+
+Argument marshalling only: every arithmetic step runs in the library's CUDA kernels (see
+``include/oqr.h`` for the contract and PAPER.md citations).  PyTorch supplies device memory
+and the stream.  There is no CPU fallback: if ``liboqr.so`` is missing or no CUDA device is
+present, calls raise.
+
+Layout: a column-major ``rows x cols`` matrix with leading dimension ``ld`` is a C-contiguous
+float64 tensor of shape ``(cols, ld)`` (element (i, j) is ``t[j, i]``) -- the same convention as
+``gen`` and the CPU checker.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboqr.so")
+NMAX = 240
+
+__all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm", "status_string",
+           "OqrError", "lib", "LIB_PATH", "NMAX", "timing_enable", "timing_reset", "timing_read",
+           "launch_count", "EXPORTS"]
+
+# Every symbol include/oqr.h declares.
+EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_status_string", "oqr_gram",
+           "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_timing_enable", "oqr_timing_reset",
+           "oqr_timing_read", "oqr_launch_count")
+
+
+class OqrError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: status {status}: {status_string(status)}")
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load liboqr.so (raises if it has not been built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with "
+                               "`python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        I64, P, I = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+        for name in ("oqr_normal", "oqr_normal2", "oqr_prequr"):
+            f = getattr(L, name)
+            f.restype = I
+            f.argtypes = [I64, I64, P, I64, P, I64, P, P, P]
+        L.oqr_status_string.restype = ctypes.c_char_p
+        L.oqr_status_string.argtypes = [I]
+        L.oqr_gram.restype = I
+        L.oqr_gram.argtypes = [I64, I64, P, I64, P, I64, P, P]
+        L.oqr_gram_euclid.restype = I
+        L.oqr_gram_euclid.argtypes = [I64, I64, P, I64, P, P]
+        L.oqr_potrf.restype = I
+        L.oqr_potrf.argtypes = [I64, P, P, P, P]
+        L.oqr_trsm.restype = I
+        L.oqr_trsm.argtypes = [I64, I64, P, I64, P, P, P]
+        L.oqr_timing_enable.restype = None
+        L.oqr_timing_enable.argtypes = [I]
+        L.oqr_timing_reset.restype = None
+        L.oqr_timing_reset.argtypes = []
+        L.oqr_timing_read.restype = I
+        L.oqr_timing_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64),
+                                      ctypes.POINTER(I64)]
+        L.oqr_launch_count.restype = I64
+        L.oqr_launch_count.argtypes = []
+        _lib = L
+    return _lib
+
+
+def status_string(status: int) -> str:
+    return lib().oqr_status_string(int(status)).decode()
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(t, name: str, rows: int | None = None):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
+        raise TypeError(f"{name}: expected a float64 CUDA tensor")
+    if t.dim() != 2 or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous 2-D tensor of shape (cols, ld)")
+    if rows is not None and t.shape[1] < rows:
+        raise ValueError(f"{name}: leading dimension {t.shape[1]} < {rows}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _variant(fname: str, A, Z, Q=None, R=None, stream=None, check: bool = True):
+    import torch
+    m = A.shape[0]
+    n = Z.shape[0]
+    pA = _check(A, "A", m)
+    pZ = _check(Z, "Z", m)
+    if Q is None:
+        Q = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    pQ = _check(Q, "Q", m)
+    pR = _check(R, "R", n)
+    if Q.shape != (n, m) or R.shape != (n, n):
+        raise ValueError("Q must be (n, m) and R (n, n)")
+    st = getattr(lib(), fname)(m, n, pA, A.shape[1], pZ, Z.shape[1], pQ, pR, _stream(stream))
+    if check and st < 0:
+        raise OqrError(st, fname)
+    return Q, R, st
+
+
+def normal(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    """CHOLQR, Algorithm 1.  Returns (Q, R, status); status > 0 is a
+    Cholesky breakdown (see include/oqr.h), negative statuses raise unless check=False."""
+    return _variant("oqr_normal", A, Z, Q, R, stream, check)
+
+
+def normal2(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    """Repeated CHOLQR: two passes, R = R2 R1 (reading R1)."""
+    return _variant("oqr_normal2", A, Z, Q, R, stream, check)
+
+
+def prequr(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    """PRE-CHOLQR, Algorithm 2 with a Euclidean Cholesky-QR pre-step."""
+    return _variant("oqr_prequr", A, Z, Q, R, stream, check)
+
+
+VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr}
+
+
+def gram(A, Z, G=None, stream=None):
+    """G = Z^T (A Z) (asynchronous step export).  Returns G as a (n, n) column-major tensor."""
+    import torch
+    m, n = A.shape[0], Z.shape[0]
+    if G is None:
+        G = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    st = lib().oqr_gram(m, n, _check(A, "A", m), A.shape[1], _check(Z, "Z", m), Z.shape[1],
+                        _check(G, "G", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_gram")
+    return G
+
+
+def gram_euclid(Z, m: int | None = None, G=None, stream=None):
+    """G = Z^T Z (asynchronous step export)."""
+    import torch
+    n = Z.shape[0]
+    m = Z.shape[1] if m is None else m
+    if G is None:
+        G = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    st = lib().oqr_gram_euclid(m, n, _check(Z, "Z", m), Z.shape[1], _check(G, "G", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_gram_euclid")
+    return G
+
+
+def potrf(G, R=None, info=None, stream=None):
+    """R = chol(G) (upper); returns (R, info tensor (1,) int32 on device)."""
+    import torch
+    n = G.shape[0]
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=G.device)
+    if info is None:
+        info = torch.zeros(1, dtype=torch.int32, device=G.device)
+    st = lib().oqr_potrf(n, _check(G, "G", n), _check(R, "R", n), ctypes.c_void_p(info.data_ptr()),
+                         _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_potrf")
+    return R, info
+
+
+def trsm(Z, R, m: int | None = None, Q=None, stream=None):
+    """Q = Z R^{-1} by row-wise substitution (asynchronous step export)."""
+    import torch
+    n = Z.shape[0]
+    m = Z.shape[1] if m is None else m
+    if Q is None:
+        Q = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+    st = lib().oqr_trsm(m, n, _check(Z, "Z", m), Z.shape[1], _check(R, "R", n), _check(Q, "Q", m),
+                        _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_trsm")
+    return Q
+
+
+def timing_enable(on: bool = True):
+    lib().oqr_timing_enable(1 if on else 0)
+
+
+def timing_reset():
+    lib().oqr_timing_reset()
+
+
+def timing_read() -> tuple[float, int, int]:
+    """(accumulated K1 milliseconds, K1 launches, all library launches) since the last reset."""
+    ms = ctypes.c_double()
+    k1 = ctypes.c_int64()
+    tot = ctypes.c_int64()
+    st = lib().oqr_timing_read(ctypes.byref(ms), ctypes.byref(k1), ctypes.byref(tot))
+    if st:
+        raise OqrError(st, "oqr_timing_read")
+    return ms.value, k1.value, tot.value
+
+
+def launch_count() -> int:
+    return int(lib().oqr_launch_count())

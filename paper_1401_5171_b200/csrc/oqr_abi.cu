@@ -1,0 +1,295 @@
+// oqr_abi.cu -- the extern "C" boundary of liboqr.so (declared in include/oqr.h).
+//
+// Host-side orchestration only: argument checks, stream-ordered workspace, kernel launches on
+// the caller's stream, the status read-back.  Every arithmetic step runs in a kernel.
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <vector>
+
+#include "../../include/oqr.h"
+#include "oqr_internal.cuh"
+
+namespace oqr {
+
+static std::atomic<int64_t> g_launches{0};
+static bool g_timing = false;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+static size_t g_event_used = 0;
+static int64_t g_timing_total_launches0 = 0;
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void timing_begin(cudaStream_t s) {
+  if (!g_timing) return;
+  if (g_event_used == g_events.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    g_events.emplace_back(a, b);
+  }
+  cudaEventRecord(g_events[g_event_used].first, s);
+}
+
+void timing_end(cudaStream_t s) {
+  if (!g_timing) return;
+  cudaEventRecord(g_events[g_event_used].second, s);
+  ++g_event_used;
+}
+
+// One pool setting per process: keep freed stream-ordered blocks cached so that the per-call
+// cudaMallocAsync/cudaFreeAsync pair costs no driver allocation after the first call.
+static void pool_keep_memory() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+// Stream-ordered scratch for one call.
+struct Workspace {
+  double* base = nullptr;
+  double* Zp = nullptr;    // packed Z (or Q1 / Y)
+  double* P = nullptr;     // per-CTA partial Gram slots
+  double* G = nullptr;     // n x n Gram
+  double* R1 = nullptr;    // n x n (R1 of normal2 / S of prequr)
+  double* R2 = nullptr;    // n x n (R2 of normal2 / U of prequr)
+  int* info = nullptr;
+  cudaStream_t s = nullptr;
+  int alloc(int64_t m, int n, cudaStream_t st) {
+    pool_keep_memory();
+    s = st;
+    const int NP = 8 * (int)cdiv(n, 8);
+    const size_t zp = (size_t)zp_doubles(m, NP);
+    const size_t sl = slots_doubles(n, gram_grid(m));
+    const size_t nn = (size_t)n * n;
+    const size_t total = zp + sl + 3 * nn + 2;  // +2 doubles (16 B) for info
+    if (cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), st) != cudaSuccess) {
+      cudaGetLastError();
+      base = nullptr;
+      return -101;
+    }
+    Zp = base;
+    P = Zp + zp;
+    G = P + sl;
+    R1 = G + nn;
+    R2 = R1 + nn;
+    info = reinterpret_cast<int*>(R2 + nn);
+    return 0;
+  }
+  ~Workspace() {
+    if (base) cudaFreeAsync(base, s);
+  }
+};
+
+static int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return 0;
+  std::fprintf(stderr, "liboqr: CUDA error: %s\n", cudaGetErrorString(e));
+  return -100;
+}
+
+#define OQR_TRY(expr)                                  \
+  do {                                                 \
+    int _st = cuda_status(expr);                       \
+    if (_st) return _st;                               \
+  } while (0)
+
+static bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static int check_args(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                      const double* Q, const double* R, bool needA, bool needQR) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m || n > OQR_NMAX) return -2;
+  if (needA) {
+    if (A == nullptr || !aligned(A, 16)) return -3;
+    if (lda < m || (lda & 1)) return -4;
+  }
+  if (Z == nullptr || !aligned(Z, 8)) return -5;
+  if (ldz < m) return -6;
+  if (needQR) {
+    if (Q == nullptr || !aligned(Q, 8)) return -7;
+    if (R == nullptr || !aligned(R, 8)) return -8;
+  }
+  return 0;
+}
+
+// G (ld n) = Z^T A Z through the packed copy of Z held in ws.Zp.
+static int gram_into(int64_t m, int n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                     double* G, Workspace& ws, cudaStream_t s) {
+  int g = 0;
+  OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
+  OQR_TRY(launch_gram_fused(m, n, A, lda, ws.Zp, ws.P, &g, s));
+  OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s));
+  return 0;
+}
+
+static int gram_euclid_into(int64_t m, int n, const double* Z, int64_t ldz, double* G, Workspace& ws,
+                            cudaStream_t s) {
+  int g = 0;
+  OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
+  OQR_TRY(launch_gram_euclid(m, n, ws.Zp, ws.P, &g, s));
+  OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s));
+  return 0;
+}
+
+// One CHOLQR pass: G = Z^T A Z; Rout = chol(G) (info = info_off + k on breakdown);
+// Q = Z Rout^{-1} (Z may be Q itself when ldz == m).
+static int cholqr_pass(int64_t m, int n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                       double* Q, double* Rout, int info_off, Workspace& ws, cudaStream_t s) {
+  int st = gram_into(m, n, A, lda, Z, ldz, ws.G, ws, s);
+  if (st) return st;
+  OQR_TRY(launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s));
+  OQR_TRY(launch_trsm(m, n, Z, ldz, Rout, n, Q, m, ws.info, s));
+  return 0;
+}
+
+static int finish(Workspace& ws, cudaStream_t s) {
+  int info = 0;
+  OQR_TRY(cudaMemcpyAsync(&info, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  OQR_TRY(cudaStreamSynchronize(s));
+  return info;
+}
+
+}  // namespace oqr
+
+using namespace oqr;
+
+extern "C" {
+
+int oqr_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+               double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int res;
+  {
+    Workspace ws;
+    if ((st = ws.alloc(m, (int)n, s))) return st;
+    st = cholqr_pass(m, (int)n, A, lda, Z, ldz, Q, R, 0, ws, s);
+    if (st) return st;
+    res = finish(ws, s);
+  }
+  return res;
+}
+
+int oqr_normal2(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int ni = (int)n;
+  Workspace ws;
+  if ((st = ws.alloc(m, ni, s))) return st;
+  // pass 1: [Q1, R1] = CHOLQR(A, Z), Q1 into Q
+  if ((st = cholqr_pass(m, ni, A, lda, Z, ldz, Q, ws.R1, 0, ws, s))) return st;
+  // pass 2: [Q, R2] = CHOLQR(A, Q1) in place; breakdown code n + k
+  if ((st = cholqr_pass(m, ni, A, lda, Q, m, Q, ws.R2, ni, ws, s))) return st;
+  // R = R2 R1
+  if ((st = cuda_status(launch_trmm(ni, ws.R2, ws.R1, R, ws.info, s)))) return st;
+  return finish(ws, s);
+}
+
+int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+               double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int ni = (int)n;
+  Workspace ws;
+  if ((st = ws.alloc(m, ni, s))) return st;
+  // pre-step: S = chol(Z^T Z), Y = Z S^{-1} (into Q)
+  if ((st = gram_euclid_into(m, ni, Z, ldz, ws.G, ws, s))) return st;
+  if ((st = cuda_status(launch_potrf(ni, ws.G, ni, ws.R1, ni, ws.info, 0, s)))) return st;
+  if ((st = cuda_status(launch_trsm(m, ni, Z, ldz, ws.R1, ni, Q, m, ws.info, s)))) return st;
+  // A-stage: [Q, U] = CHOLQR(A, Y) in place; breakdown code n + k
+  if ((st = cholqr_pass(m, ni, A, lda, Q, m, Q, ws.R2, ni, ws, s))) return st;
+  // R = U S
+  if ((st = cuda_status(launch_trmm(ni, ws.R2, ws.R1, R, ws.info, s)))) return st;
+  return finish(ws, s);
+}
+
+const char* oqr_status_string(int status) {
+  if (status == 0) return "success";
+  if (status > 0) return "Cholesky breakdown (pivot <= 0 or NaN); code k: first Cholesky, n+k: second";
+  switch (status) {
+    case -1: return "invalid argument 1 (m < 1)";
+    case -2: return "invalid argument 2 (n < 1, n > m or n > OQR_NMAX)";
+    case -3: return "invalid argument 3 (A null or not 16-byte aligned)";
+    case -4: return "invalid argument 4 (lda < m or odd)";
+    case -5: return "invalid argument 5 (Z null or not 8-byte aligned)";
+    case -6: return "invalid argument 6 (ldz < m)";
+    case -7: return "invalid argument 7 (Q null or not 8-byte aligned)";
+    case -8: return "invalid argument 8 (R null or not 8-byte aligned)";
+    case -100: return "CUDA error";
+    case -101: return "workspace allocation failed";
+    default: return "unknown status";
+  }
+}
+
+int oqr_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+             double* G, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, nullptr, nullptr, true, false);
+  if (st) return st;
+  if (G == nullptr) return -7;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws;
+  if ((st = ws.alloc(m, (int)n, s))) return st;
+  return gram_into(m, (int)n, A, lda, Z, ldz, G, ws, s);
+}
+
+int oqr_gram_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* G, oqr_stream_t stream) {
+  int st = check_args(m, n, nullptr, m, Z, ldz, nullptr, nullptr, false, false);
+  if (st) return st;
+  if (G == nullptr) return -7;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws;
+  if ((st = ws.alloc(m, (int)n, s))) return st;
+  return gram_euclid_into(m, (int)n, Z, ldz, G, ws, s);
+}
+
+int oqr_potrf(int64_t n, const double* G, double* R, int* d_info, oqr_stream_t stream) {
+  if (n < 1 || n > OQR_NMAX) return -2;
+  if (G == nullptr || R == nullptr || d_info == nullptr) return -3;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return cuda_status(launch_potrf((int)n, G, n, R, n, d_info, 0, s));
+}
+
+int oqr_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, double* Q,
+             oqr_stream_t stream) {
+  int st = check_args(m, n, nullptr, m, Z, ldz, Q, R, false, true);
+  if (st) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return cuda_status(launch_trsm(m, (int)n, Z, ldz, R, n, Q, m, nullptr, s));
+}
+
+void oqr_timing_enable(int enable) { g_timing = enable != 0; }
+
+void oqr_timing_reset(void) {
+  g_event_used = 0;
+  g_timing_total_launches0 = g_launches.load();
+}
+
+int oqr_timing_read(double* gram_ms, int64_t* gram_launches, int64_t* total_launches) {
+  double ms = 0.0;
+  for (size_t i = 0; i < g_event_used; ++i) {
+    if (cudaEventSynchronize(g_events[i].second) != cudaSuccess) return -100;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, g_events[i].first, g_events[i].second) != cudaSuccess) return -100;
+    ms += t;
+  }
+  if (gram_ms) *gram_ms = ms;
+  if (gram_launches) *gram_launches = (int64_t)g_event_used;
+  if (total_launches) *total_launches = g_launches.load() - g_timing_total_launches0;
+  return 0;
+}
+
+int64_t oqr_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// oqr_internal.cuh -- shared constants, PTX wrappers and launchers of liboqr (sm_100a only).
+//
+// Nothing here is shared with oracle/ (the CPU checker); see DESIGN.md s3.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "liboqr is written for sm_100a (B200) only"
+#endif
+
+namespace oqr {
+
+// ---- Tiling of the fused Gram kernel (K1) and its packed Z layout ----------
+constexpr int BM = 64;        // rows of A (and of W = AZ) per panel: 8 consumer warps x 8 rows
+constexpr int BK = 16;        // columns of A (k of AZ) per pipeline stage
+constexpr int AS = BM + 4;    // smem stride (doubles) of one staged A column: with 64-bit
+                              // fragment loads, 4*k + r covers 16 distinct 8-byte banks
+constexpr int ZS = BK + 4;    // stride (doubles) of one column of a packed Z block (same rule)
+constexpr int NCW = 8;        // consumer (DMMA) warps per CTA
+constexpr int LG = 4;         // n-tiles per contraction chunk (cross-warp reduction granule)
+constexpr int NTMAX = 30;     // n <= 8 * NTMAX = 240 = OQR_NMAX
+constexpr int SMEM_MAX = 227 * 1024;
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Packed Z ("Zp"): block b holds rows [b*BK, b*BK+BK) of Z as NP columns of ZS doubles,
+//   Zp[(b*NP + l)*ZS + kk] = Z[b*BK + kk, l]   (zero for kk >= BK, rows >= m, l >= n),
+// so one pipeline stage's Z tile is a single contiguous bulk copy, already in the padded,
+// bank-conflict-free smem layout.  Blocks cover every panel row: nblk = ceil(m/BM)*BM/BK.
+inline int64_t zp_blocks(int64_t m) { return cdiv(m, BM) * (BM / BK); }
+inline int64_t zp_doubles(int64_t m, int NP) { return zp_blocks(m) * NP * ZS; }
+
+// ---- launch bookkeeping (oqr_abi.cu) ----
+void note_launch();
+void timing_begin(cudaStream_t s);
+void timing_end(cudaStream_t s);
+
+// ---- launchers (return cudaError_t of the launch) ----
+// Z (m x n, ldz) -> Zp (packed, NP = 8*ceil(n/8) columns)
+cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s);
+// Per-CTA partial Gram slots P[g][NP][NP] of Z^T (A Z); returns the grid size used in *g_out.
+cudaError_t launch_gram_fused(int64_t m, int n, const double* A, int64_t lda, const double* Zp,
+                              double* P, int* g_out, cudaStream_t s);
+// Per-CTA partial slots of Z^T Z.
+cudaError_t launch_gram_euclid(int64_t m, int n, const double* Zp, double* P, int* g_out,
+                               cudaStream_t s);
+// G (n x n, ldg) = sum_{c<g} P[c] in fixed c order.
+cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s);
+// R = chol(G) (upper); *info = 0 | k (info_off == 0), or (only if *info == 0) n + k.
+cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
+                         int info_off, cudaStream_t s);
+// Q = Z R^{-1}; skipped when info != nullptr && *info != 0.
+cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
+                        double* Q, int64_t ldq, const int* info, cudaStream_t s);
+// R = R2 * R1 (upper x upper); skipped when *info != 0.
+cudaError_t launch_trmm(int n, const double* R2, const double* R1, double* R, const int* info,
+                        cudaStream_t s);
+
+// Workspace size (bytes) for the Gram of an (m, n) problem on a grid of g CTAs.
+int gram_grid(int64_t m);
+size_t slots_doubles(int n, int g);
+
+}  // namespace oqr

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Gates T1-T8 of SURVEY.md s8(c) / DESIGN.md s5, each tolerance derived from the
+paper's error model with c = 1:
+
+  T1 Gram        |G_gpu - G_orc| <= 2 gamma_{3m} |Z|^T|A||Z|        (eq.mult1-2, any sum order)
+  T2 repr.       rho_gpu = max |Z-QR| / (|Q||R|) <= gamma_{n+1}      (Thm 2 componentwise)
+  T3 Cholesky    |G - R^T R| <= gamma_{n+1} |R|^T|R|                 (eq:normal:chol)
+  T4 trsm        rho(Z, Q, R) <= gamma_{n+1} for given (Z, R)
+  T5 orth.       E_gpu <= 10 E_orc + 10 n u ||A|| ||Q_orc||^2        (Thms 2-3)
+  T6 forward     ||X_gpu - X_orc||_F / ||X_orc||_F <= sqrt(m) u kappa(G)   X in {R, Q}
+  T7 outcome     same status class (0 / first Cholesky / second Cholesky)
+  T8 determinism two runs bitwise equal
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from oracle import U, gamma
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def oqr():
+    import paper_1401_5171_b200 as m
+    m.lib()
+    return m
+
+
+DEV = "cuda:0"
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# shapes spanning several 64-row panels and 16-column k-blocks, ragged tails, n not a multiple
+# of 8, n = 1, n = m, n = OQR_NMAX, padded leading dimensions.
+SHAPES = [
+    # (m, n, kappa_A, kappa_Z, seed, lda_pad, ldz_pad)
+    (200, 10, 1e2, 1e2, gen.SEED_BASE + 0, 0, 0),      # config 0
+    (333, 21, 1e3, 1e2, 11, 0, 0),                      # ragged panel + ragged k-block (odd m)
+    (1000, 100, 1e2, 1e2, 12, 8, 3),                    # padded lda / odd ldz
+    (1031, 1, 1e4, 1.0, 13, 2, 0),                      # n = 1, m prime
+    (96, 96, 1e2, 1e2, 14, 0, 0),                       # n = m
+    (517, 240, 1e2, 1e2, 15, 0, 0),                     # n = OQR_NMAX, ragged
+    (4000, 50, 1e4, 1e3, gen.SEED_BASE + 1, 0, 0),      # config 1
+]
+
+
+def make(m, n, ka, kz, seed, lda_pad=0, ldz_pad=0, ucase="reflect"):
+    return gen.problem(m, n, ka, kz, seed, ucase=ucase, lda=m + lda_pad, ldz=m + ldz_pad)
+
+
+def check_gram(oqr, p):
+    m = p.m
+    G = host(oqr.gram(to_dev(p.A), to_dev(p.Z)))
+    Gd, M = oracle.dd_gram(p.A, p.Z, m)       # dense n x n, double-double G and |Z|^T|A||Z|
+    Go = oracle.from_cm(oracle.gram(p.A, p.Z, m), p.n)
+    Gg = G.T                                  # storage (n, n) col-major -> dense
+    tol = 2 * gamma(3 * m) * M
+    assert np.all(np.abs(Gg - Go) <= tol), np.max(np.abs(Gg - Go) / M)
+    assert np.all(np.abs(Gg - Gd) <= gamma(3 * m) * M)
+    return G
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_t1_gram(oqr, shape):
+    check_gram(oqr, make(*shape))
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_t1_gram_euclid(oqr, shape):
+    p = make(*shape)
+    m, n = p.m, p.n
+    G = host(oqr.gram_euclid(to_dev(p.Z), m=m)).T
+    Go = oracle.from_cm(oracle.gram_euclid(p.Z, m), n)
+    Zd = oracle.from_cm(p.Z, m)
+    M = np.abs(Zd).T @ np.abs(Zd)
+    assert np.all(np.abs(G - Go) <= 2 * gamma(3 * m) * M)
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_t3_potrf(oqr, shape):
+    p = make(*shape)
+    n = p.n
+    G = oracle.gram(p.A, p.Z, p.m)            # oracle G (storage (n, n))
+    R, info = oqr.potrf(to_dev(G))
+    assert int(host(info)[0]) == 0
+    Rg = host(R)
+    ratio = oracle.chol_backward_ratio(oracle.from_cm(G, n), Rg)
+    assert ratio <= gamma(n + 1), ratio / U
+    Ro, io = oracle.potrf(G)
+    assert io == 0
+    assert np.all(np.tril(oracle.from_cm(Rg, n), -1) == 0)
+    kG = np.linalg.cond(oracle.from_cm(G, n))
+    assert np.linalg.norm(Rg - Ro) / np.linalg.norm(Ro) <= math.sqrt(p.m) * U * kG
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_t4_trsm(oqr, shape):
+    p = make(*shape)
+    m, n = p.m, p.n
+    R, _ = oracle.potrf(oracle.gram(p.A, p.Z, m))
+    Q = host(oqr.trsm(to_dev(p.Z), to_dev(R), m=m))
+    rho = oracle.componentwise_ratio(p.Z, Q, R, m)
+    assert rho <= gamma(n + 1), rho / U
+    Qo = oracle.trsm(p.Z, R, m)
+    kR = np.linalg.cond(oracle.from_cm(R, n))
+    assert np.linalg.norm(Q - Qo) / np.linalg.norm(Qo) <= math.sqrt(m) * U * kR
+
+
+def test_potrf_breakdown_examples(oqr):
+    # [[1,2],[2,1]] breaks down at pivot 2; NaN pivot breaks down (reading R4)
+    G = oracle.to_cm(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    _, info = oqr.potrf(to_dev(G))
+    assert int(host(info)[0]) == 2
+    G = np.eye(3)
+    G[1, 1] = np.nan
+    _, info = oqr.potrf(to_dev(oracle.to_cm(G)))
+    assert int(host(info)[0]) == 2
+    G = oracle.to_cm(np.array([[4.0, 2.0], [2.0, 5.0]]))
+    R, info = oqr.potrf(to_dev(G))
+    assert int(host(info)[0]) == 0
+    assert np.array_equal(oracle.from_cm(host(R), 2), np.array([[2.0, 1.0], [0.0, 2.0]]))
+
+
+def variant_gates(oqr, p, variant):
+    m, n = p.m, p.n
+    Q, R, st = oqr.VARIANTS[variant](to_dev(p.A), to_dev(p.Z))
+    Qo, Ro, sto = oracle.VARIANTS[variant](p.A, p.Z, m)
+    cls = lambda s: 0 if s == 0 else (1 if s <= n else 2)
+    assert cls(st) == cls(sto), (st, sto)                      # T7
+    if st != 0:
+        return None
+    Qg, Rg = host(Q), host(R)
+    assert np.all(np.tril(oracle.from_cm(Rg, n), -1) == 0)
+    assert np.all(np.diag(oracle.from_cm(Rg, n)) > 0)
+    rho = oracle.componentwise_ratio(p.Z, Qg, Rg, m)           # T2
+    rho_o = oracle.componentwise_ratio(p.Z, Qo, Ro, m)
+    if variant == "normal":
+        assert rho <= gamma(n + 1), rho / U
+    else:
+        assert rho <= 10 * rho_o + 4 * gamma(n + 1), (rho / U, rho_o / U)
+    e = oracle.orth_error(p.A, Qg, m)                          # T5
+    eo = oracle.orth_error(p.A, Qo, m)
+    normA = float(np.max(p.d))                                  # ||A||_2 (generator ground truth)
+    normQ = np.linalg.norm(oracle.from_cm(Qo, m), 2)
+    assert e <= 10 * eo + 10 * n * U * normA * normQ ** 2, (e, eo)
+    G = oracle.from_cm(oracle.gram(p.A, p.Z, m), n)             # T6
+    kG = np.linalg.cond(G)
+    assert np.linalg.norm(Rg - Ro) / np.linalg.norm(Ro) <= math.sqrt(m) * U * kG
+    assert np.linalg.norm(Qg - Qo) / np.linalg.norm(Qo) <= math.sqrt(m) * U * kG
+    return Qg, Rg, st
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_t2_t5_t6_t7_variants(oqr, shape, variant):
+    variant_gates(oqr, make(*shape), variant)
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+def test_t8_determinism(oqr, variant):
+    p = make(4000, 50, 1e4, 1e3, 99)
+    A, Z = to_dev(p.A), to_dev(p.Z)
+    Q1, R1, s1 = oqr.VARIANTS[variant](A, Z)
+    Q2, R2, s2 = oqr.VARIANTS[variant](A, Z)
+    assert s1 == s2 == 0
+    assert torch.equal(Q1, Q2) and torch.equal(R1, R2)
+    G1 = oqr.gram(A, Z)
+    G2 = oqr.gram(A, Z)
+    assert torch.equal(G1, G2)
+
+
+@pytest.mark.parametrize("ucase", ["top", "bottom", "split", "aorth"])
+def test_paper_cases_small(oqr, ucase):
+    # the paper's s7 constructions at m = 80, n = 10
+    for ka in (1e2, 1e6, 1e10):
+        p = gen.problem(80, 10, ka, math.sqrt(ka), 5, ucase=ucase)
+        for v in ("normal", "normal2", "prequr"):
+            variant_gates(oqr, p, v)
+
+
+def test_breakdown_witness_small(oqr):
+    # paper case 3 with kappa(A^{1/2}Z)^2 = kappa(G) = 1e20 >> 1/u: CHOLQR must break down in its
+    # (first) Cholesky, normal2 in pass 1; prequr still succeeds (s8(c) item 14)
+    p = gen.problem(400, 20, 1e8, 1e6, 77, ucase="split")
+    A, Z = to_dev(p.A), to_dev(p.Z)
+    _, _, st = oqr.normal(A, Z)
+    _, _, sto = oracle.normal(p.A, p.Z, p.m)
+    assert 1 <= st <= p.n and 1 <= sto <= p.n
+    _, _, st2 = oqr.normal2(A, Z)
+    assert 1 <= st2 <= p.n
+    variant_gates(oqr, p, "prequr")
+
+
+def test_nan_input_breaks_down(oqr):
+    p = make(300, 12, 1e2, 1e2, 3)
+    Z = p.Z.copy()
+    Z[4, 17] = np.nan
+    _, _, st = oqr.normal(to_dev(p.A), to_dev(Z))
+    assert 1 <= st <= p.n
+
+
+def test_abi_argument_errors_on_device(oqr):
+    p = make(64, 8, 1e2, 1e2, 1)
+    A, Z = to_dev(p.A), to_dev(p.Z)
+    Q = torch.empty((8, 64), dtype=torch.float64, device=DEV)
+    R = torch.empty((8, 8), dtype=torch.float64, device=DEV)
+    import ctypes
+    L = oqr.lib()
+    P = ctypes.c_void_p
+    s = P(torch.cuda.current_stream().cuda_stream)
+    assert L.oqr_normal(64, 8, P(A.data_ptr() + 8), 64, P(Z.data_ptr()), 64, P(Q.data_ptr()), P(R.data_ptr()), s) == -3
+    assert L.oqr_normal(64, 8, P(A.data_ptr()), 64, P(Z.data_ptr()), 64, P(Q.data_ptr()), P(R.data_ptr()), s) == 0
+
+
+def test_stream_and_launch_accounting(oqr):
+    p = make(500, 30, 1e2, 1e2, 2)
+    A, Z = to_dev(p.A), to_dev(p.Z)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        n0 = oqr.launch_count()
+        Q, R, s = oqr.normal(A, Z)
+        assert s == 0
+        assert oqr.launch_count() - n0 == 5          # pack, K1, K1r, K2, K3
+    Qo, Ro, _ = oracle.normal(p.A, p.Z, p.m)
+    assert np.linalg.norm(host(R) - Ro) / np.linalg.norm(Ro) < 1e-12
