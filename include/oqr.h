@@ -15,8 +15,9 @@
  *    leading dimension ld is p[j*ld + i].  All matrix pointers are DEVICE pointers owned by
  *    the caller; the library never frees or retains them.
  *  - A is read in full as given (both triangles); it is never written.  Z is never written.
- *  - lda, ldz >= m and EVEN; A and Z 16-byte aligned (the kernels move A columns with
- *    cp.async.bulk, which needs 16-byte aligned sources).
+ *  - lda, ldz >= m; all pointers 8-byte aligned.  FAST PATH: A 16-byte aligned and lda even --
+ *    the fused Gram kernel then moves A columns with cp.async.bulk (16-byte aligned sources);
+ *    otherwise it falls back to plain loads for every tile (same results, much slower).
  *  - 1 <= n <= min(m, OQR_NMAX).
  *  - Q: m x n output with leading dimension m.  R: n x n output with leading dimension n,
  *    upper triangular with positive diagonal; its strictly lower part is written as zero.
@@ -32,8 +33,8 @@
  *              breaks down when it is <= 0 or NaN (reading R4).
  *     n+1..2n  breakdown at pivot k of the SECOND Cholesky (pass 2 of oqr_normal2, the
  *              A-stage of oqr_prequr); the code is n + k (LAPACK xSYGV's INFO = N + i idiom).
- *    -i        argument i is invalid: -1 m, -2 n, -3 A (null or misaligned), -4 lda (< m or
- *              odd), -5 Z, -6 ldz, -7 Q, -8 R.  Nothing is launched.
+ *    -i        argument i is invalid: -1 m, -2 n, -3 A (null or not 8-byte aligned), -4 lda
+ *              (< m), -5 Z, -6 ldz, -7 Q, -8 R.  Nothing is launched.
  *   -100       a CUDA error occurred (launch or runtime); -101 workspace allocation failed.
  *  On any nonzero status the contents of Q and R are unspecified.
  *

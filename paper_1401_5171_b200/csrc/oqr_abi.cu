@@ -108,8 +108,8 @@ static int check_args(int64_t m, int64_t n, const double* A, int64_t lda, const 
   if (m < 1) return -1;
   if (n < 1 || n > m || n > OQR_NMAX) return -2;
   if (needA) {
-    if (A == nullptr || !aligned(A, 16)) return -3;
-    if (lda < m || (lda & 1)) return -4;
+    if (A == nullptr || !aligned(A, 8)) return -3;
+    if (lda < m) return -4;
   }
   if (Z == nullptr || !aligned(Z, 8)) return -5;
   if (ldz < m) return -6;
@@ -221,8 +221,8 @@ const char* oqr_status_string(int status) {
   switch (status) {
     case -1: return "invalid argument 1 (m < 1)";
     case -2: return "invalid argument 2 (n < 1, n > m or n > OQR_NMAX)";
-    case -3: return "invalid argument 3 (A null or not 16-byte aligned)";
-    case -4: return "invalid argument 4 (lda < m or odd)";
+    case -3: return "invalid argument 3 (A null or not 8-byte aligned)";
+    case -4: return "invalid argument 4 (lda < m)";
     case -5: return "invalid argument 5 (Z null or not 8-byte aligned)";
     case -6: return "invalid argument 6 (ldz < m)";
     case -7: return "invalid argument 7 (Q null or not 8-byte aligned)";

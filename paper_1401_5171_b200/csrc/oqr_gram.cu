@@ -157,21 +157,21 @@ __device__ __forceinline__ void contract_panel(double (&acc)[NT][2], int64_t row
           *reinterpret_cast<double2*>(red + (warp * LG + j) * 64 + lane * 2) = make_double2(o[0], o[1]);
         }
       }
+      // this thread's output entry of the chunk (LG*64 == NCW*32: exactly one per thread);
+      // its previous slot value is fetched before the barrier so the L2 latency overlaps it
+      static_assert(LG * 64 == NCW * 32, "one chunk entry per consumer thread");
+      const int v = ctid;
+      const int j = v >> 6;
+      const int lt = lg * LG + j;
+      const int t = (v & 63) >> 1, e = v & 1;
+      double* p = slot + (int64_t)(lt * 8 + 2 * (t & 3) + e) * NP + kt * 8 + (t >> 2);
+      const double prev = (!first && lt < NT) ? *p : 0.0;
       named_bar_sync(1, NCW * 32);
+      if (lt < NT) {
+        double s = red[j * 64 + (v & 63)];
 #pragma unroll
-      for (int v = ctid; v < LG * 64; v += NCW * 32) {
-        const int j = v >> 6;
-        const int lt = lg * LG + j;
-        if (lt < NT) {
-          const int t = (v & 63) >> 1, e = v & 1;
-          double s = red[j * 64 + (v & 63)];
-#pragma unroll
-          for (int w = 1; w < NCW; ++w) s += red[(w * LG + j) * 64 + (v & 63)];
-          const int k = kt * 8 + (t >> 2);
-          const int l = lt * 8 + 2 * (t & 3) + e;
-          double* p = slot + (int64_t)l * NP + k;
-          *p = first ? s : (*p + s);
-        }
+        for (int w = 1; w < NCW; ++w) s += red[(w * LG + j) * 64 + (v & 63)];
+        *p = first ? s : (prev + s);
       }
       named_bar_sync(1, NCW * 32);
     }
@@ -181,34 +181,46 @@ __device__ __forceinline__ void contract_panel(double (&acc)[NT][2], int64_t row
 // ------------------------------------------------------------------ K1 --------------------
 // Fill ring slot `s` with unit u = (panel I, k-block kb): BK columns of A (rows I*BM..+BM, one
 // 512 B bulk copy per column into a padded smem column) and the packed Z block kb (one bulk
-// copy).  Executed by all 32 lanes of warp 0.  A ragged panel / k-block (the last of each; only
-// when m is not a multiple of BM / BK) is loaded with plain loads and zero fill instead.
+// copy).  Executed by all 32 lanes of warp 0.
+// Ragged tiles (last panel / last k-block when m is not a multiple of BM / BK): only the valid
+// rows and columns are copied; the rest of the slot keeps finite stale data (the ring is zeroed
+// at kernel start), which only ever meets the zero rows of the packed Z (rows >= m), so it adds
+// exactly 0.  Bulk copies move multiples of 16 B, so an odd count of valid rows copies one row
+// fewer and the last row is loaded with plain loads.  When A's columns are not 16-byte aligned
+// (odd lda or an 8-byte aligned A) every tile is loaded with plain loads (correct, slow).
 template <int NT>
 __device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, const double* __restrict__ A,
                                             int64_t lda, const double* __restrict__ Zp, double* As,
-                                            uint64_t* bar, int lane, uint64_t pol_a, uint64_t pol_z) {
+                                            uint64_t* bar, int lane, uint64_t pol_a, uint64_t pol_z,
+                                            bool bulk_ok) {
   constexpr int NP = NT * 8;
   constexpr uint32_t zbytes = NP * ZS * 8;
   const int64_t I = u / KB, kb = u - I * KB;
   const int64_t row0 = I * BM, col0 = kb * BK;
   double* Zs = As + BK * AS;
   const double* zsrc = Zp + kb * (int64_t)(NP * ZS);
-  if (row0 + BM <= m && col0 + BK <= m) {
-    if (lane == 0) mbar_arrive_expect_tx(bar, zbytes + BK * BM * 8);
+  const int rows = (int)(m - row0 < BM ? m - row0 : BM);
+  const int cols = (int)(m - col0 < BK ? m - col0 : BK);
+  if (bulk_ok) {
+    const int rows_bulk = rows & ~1;
+    if (rows_bulk != rows && lane < cols)  // odd valid-row count: last row by plain loads
+      As[lane * AS + rows - 1] = A[(col0 + lane) * lda + row0 + rows - 1];
+    fence_proxy_async_smem();  // order these generic writes before later bulk writes to the slot
     __syncwarp();
-    if (lane < BK)
-      bulk_g2s(As + lane * AS, A + (col0 + lane) * lda + row0, BM * 8, bar, pol_a);
+    if (lane == 0) mbar_arrive_expect_tx(bar, zbytes + (uint32_t)(cols * rows_bulk * 8));
+    __syncwarp();
+    if (lane < cols && rows_bulk > 0)
+      bulk_g2s(As + lane * AS, A + (col0 + lane) * lda + row0, rows_bulk * 8, bar, pol_a);
     else if (lane == BK)
       bulk_g2s(Zs, zsrc, zbytes, bar, pol_z);
   } else {
     for (int e = lane; e < BK * BM; e += 32) {
       const int k = e / BM, r = e - k * BM;
       double v = 0.0;
-      if (row0 + r < m && col0 + k < m) v = A[(col0 + k) * lda + row0 + r];
+      if (r < rows && k < cols) v = A[(col0 + k) * lda + row0 + r];
       As[k * AS + r] = v;
     }
-    __threadfence_block();
-    fence_proxy_async_smem();  // generic writes before later async-proxy (bulk) writes to the slot
+    fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
       mbar_arrive_expect_tx(bar, zbytes);
@@ -225,7 +237,7 @@ __device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, co
 template <int NT>
 __global__ void __launch_bounds__(NCW * 32, 1)
 gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const double* __restrict__ Zp,
-                  double* __restrict__ P, int64_t KB, int64_t U, int stages) {
+                  double* __restrict__ P, int64_t KB, int64_t U, int stages, bool bulk_ok) {
   constexpr int NP = NT * 8;
   constexpr int STAGE = BK * AS + NP * ZS;  // doubles per pipeline stage
   extern __shared__ __align__(128) unsigned char smem[];
@@ -238,6 +250,9 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
   const int64_t g = gridDim.x, c = blockIdx.x;
   const int64_t u0 = U * c / g, u1 = U * (c + 1) / g;
 
+  // zero the ring once: slots of ragged tiles keep finite data outside their valid region
+  for (int e = threadIdx.x; e < stages * STAGE; e += blockDim.x) ring[e] = 0.0;
+  fence_proxy_async_smem();  // generic zero-fill before the async-proxy (bulk) writes
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
@@ -252,7 +267,7 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
     pol_a = policy_evict_first();  // A is streamed exactly once
     pol_z = policy_evict_last();   // Zp is re-read by every panel
     for (int s = 0; s < stages && u0 + s < u1; ++s)
-      issue_stage<NT>(u0 + s, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z);
+      issue_stage<NT>(u0 + s, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, bulk_ok);
   }
 
   double* slot = P + c * (int64_t)NP * NP;
@@ -281,7 +296,7 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
     if (lane == 0) mbar_arrive(&empty[s]);
     if (warp == 0 && u + stages < u1) {
       mbar_wait(&empty[s], ph);
-      issue_stage<NT>(u + stages, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z);
+      issue_stage<NT>(u + stages, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, bulk_ok);
     }
     if (++s == stages) {
       s = 0;
@@ -387,7 +402,8 @@ static cudaError_t gram_fused_nt(int64_t m, const double* A, int64_t lda, const 
   if (g > U) g = U;
   *g_out = (int)g;
   timing_begin(s);
-  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(m, A, lda, Zp, P, KB, U, stages);
+  const bool bulk_ok = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
+  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(m, A, lda, Zp, P, KB, U, stages, bulk_ok);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);

@@ -54,8 +54,10 @@ def test_library_is_sm100a_only(L):
 
 def test_sass_uses_fp64_tensor_pipe_and_bulk_copy(L):
     import paper_1401_5171_b200 as oqr
-    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                          "_ZN3oqr17gram_fused_kernelILi25EEEvlPKdlS2_Pdlli", oqr.LIB_PATH],
+    syms = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-symbols", oqr.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    name = re.search(r"(_ZN3oqr17gram_fused_kernelILi25EE\w+)", syms).group(1)
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun", name, oqr.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "DMMA" in out            # mma.sync f64 -> FP64 tensor pipe
     assert "UBLKCP" in out          # cp.async.bulk -> bulk-copy (TMA) engine
@@ -68,12 +70,12 @@ def test_sass_uses_fp64_tensor_pipe_and_bulk_copy(L):
     ((10, 11, 16, 10, 16, 10, 16, 16), -2),
     ((300, 241, 16, 300, 16, 300, 16, 16), -2),
     ((10, 2, 0, 10, 16, 10, 16, 16), -3),
-    ((10, 2, 8, 10, 16, 10, 16, 16), -3),     # A not 16-byte aligned
+    ((10, 2, 4, 10, 16, 10, 16, 16), -3),     # A not 8-byte aligned
     ((10, 2, 16, 9, 16, 10, 16, 16), -4),     # lda < m
-    ((10, 2, 16, 11, 16, 10, 16, 16), -4),    # lda odd
     ((10, 2, 16, 10, 0, 10, 16, 16), -5),
     ((10, 2, 16, 10, 16, 9, 16, 16), -6),
     ((10, 2, 16, 10, 16, 10, 0, 16), -7),
+    ((10, 2, 16, 10, 16, 10, 12, 16), -7),    # Q not 8-byte aligned
     ((10, 2, 16, 10, 16, 10, 16, 0), -8),
 ])
 @pytest.mark.parametrize("fn", ["oqr_normal", "oqr_normal2", "oqr_prequr"])
