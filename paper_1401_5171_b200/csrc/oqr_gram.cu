@@ -231,9 +231,9 @@ __device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, co
 }
 
 // 8 warps, one CTA per SM (2 warps per SM sub-partition => up to 255 registers per thread).
-// Every warp owns 8 rows of W_I (all NP columns) in DMMA accumulators; warp 0 also refills the
-// ring: after all 8 warps released slot s (empty barrier) it issues the copies for the unit
-// `stages` ahead, so `stages - 1` stages of compute cover the copy latency.
+// Every warp owns 8 rows of W_I (all NP columns) in DMMA accumulators.  Warp 0 fills the ring
+// initially; afterwards whichever warp releases slot s last refills it with the unit `stages`
+// ahead, so `stages - 1` stages of compute cover the copy latency.
 template <int NT>
 __global__ void __launch_bounds__(NCW * 32, 1)
 gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const double* __restrict__ Zp,
@@ -243,7 +243,8 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
-  double* red = reinterpret_cast<double*>(smem + 128);
+  unsigned* relcnt = reinterpret_cast<unsigned*>(empty + 8);  // 8 release counters (32 B)
+  double* red = reinterpret_cast<double*>(smem + 192);
   double* ring = red + NCW * LG * 64;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,15 +258,15 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
+      relcnt[s] = 0u;
     }
     mbar_fence_init();
   }
   __syncthreads();
 
-  uint64_t pol_a = 0, pol_z = 0;
+  const uint64_t pol_a = policy_evict_first();  // A is streamed exactly once
+  const uint64_t pol_z = policy_evict_last();   // Zp is re-read by every panel
   if (warp == 0) {
-    pol_a = policy_evict_first();  // A is streamed exactly once
-    pol_z = policy_evict_last();   // Zp is re-read by every panel
     for (int s = 0; s < stages && u0 + s < u1; ++s)
       issue_stage<NT>(u0 + s, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, bulk_ok);
   }
@@ -293,8 +294,16 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (warp == 0 && u + stages < u1) {
+    // release the slot; the LAST warp to release it refills it at once (no warp is paced by
+    // another's compute).  The arrival counter only elects that warp; the empty mbarrier's
+    // acquire then orders all eight warps' reads of the slot before the new bulk writes.
+    int last = 0;
+    if (lane == 0) {
+      mbar_arrive(&empty[s]);
+      last = (atomicAdd(&relcnt[s], 1u) % NCW) == NCW - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && u + stages < u1) {
       mbar_wait(&empty[s], ph);
       issue_stage<NT>(u + stages, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, bulk_ok);
     }
@@ -378,7 +387,7 @@ size_t slots_doubles(int n, int g) {
 
 static int fused_stages(int NT, size_t* bytes) {
   const size_t stage = (size_t)(BK * AS + NT * 8 * ZS) * 8;
-  const size_t fixed = 128 + (size_t)NCW * LG * 64 * 8;
+  const size_t fixed = 192 + (size_t)NCW * LG * 64 * 8;
   int st = (int)((SMEM_MAX - fixed) / stage);
   if (st > 8) st = 8;
   *bytes = fixed + st * stage;
