@@ -11,8 +11,14 @@
 //
 // FP64 has no tcgen05 kind on sm_100a (ptxas rejects .kind::f64); the FP64 tensor pipe is
 // reached through warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Operands are staged in
-// shared memory by the bulk-copy engine (cp.async.bulk -> SASS UBLKCP) through an mbarrier
-// ring fed by one producer warp; 8 consumer warps each own 8 rows of W_I in registers.
+// shared memory through an mbarrier ring: the A tile (64 rows x 16 columns) by ONE 2-D tensor
+// TMA request (SASS UTMALDG; out-of-bounds rows/columns are zero-filled by the hardware), the
+// packed Z block by one 1-D bulk copy (SASS UBLKCP).  16 warps per CTA (8 row groups x 2
+// column halves) keep W_I in DMMA accumulators.
+#include <cuda.h>  // CUtensorMap and its enums (the encode entry point is fetched at run time)
+
+#include <cstring>
+
 #include "oqr_internal.cuh"
 
 namespace oqr {
@@ -69,158 +75,171 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// 2-D tensor TMA global -> shared (box of the tensor map at coordinates {c0, c1}).
+__device__ __forceinline__ void tma_g2s_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                           uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 // D = A * B + D on the FP64 tensor pipe.  A: 8x4 row (lane: row lane/4, col lane%4),
 // B: 4x8 col (lane: row lane%4, col lane/4), D: 8x8 (lane: row lane/4, cols 2*(lane%4)+{0,1}).
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+#ifdef OQR_EXP_NODMMA  // experiment build only (tools/exp): keeps the operand loads, drops DMMA
+  d[0] += a;
+  d[1] += b;
+  return;
+#endif
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
 
 // ------------------------------------------------------------------ Z packing -------------
-__global__ void pack_z_kernel(int64_t m, int n, int NP, const double* __restrict__ Z, int64_t ldz,
+// Zp[((b*NT + lt)*4 + kk)*32 + ln] = Z[b*BK + kk*4 + ln%4, lt*8 + ln/4] (zero outside Z).
+__global__ void pack_z_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t ldz,
                               double* __restrict__ Zp, int64_t total) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int kk = (int)(e % ZS);
-    const int64_t bl = e / ZS;
-    const int l = (int)(bl % NP);
-    const int64_t b = bl / NP;
-    const int64_t row = b * BK + kk;
+    const int ln = (int)(e & 31);
+    const int64_t f = e >> 5;
+    const int kk = (int)(f & 3);
+    const int64_t bl = f >> 2;
+    const int lt = (int)(bl % NT);
+    const int64_t b = bl / NT;
+    const int64_t row = b * BK + kk * 4 + (ln & 3);
+    const int col = lt * 8 + (ln >> 2);
     double v = 0.0;
-    if (kk < BK && row < m && l < n) v = Z[(int64_t)l * ldz + row];
+    if (row < m && col < n) v = Z[(int64_t)col * ldz + row];
     Zp[e] = v;
   }
 }
 
 cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s) {
-  const int NP = 8 * (int)cdiv(n, 8);
-  const int64_t total = zp_doubles(m, NP);
+  const int NT = (int)cdiv(n, 8);
+  const int64_t total = zp_doubles(m, 8 * NT);
   int64_t blocks = cdiv(total, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  pack_z_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, n, NP, Z, ldz, Zp, total);
+  pack_z_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, n, NT, Z, ldz, Zp, total);
   note_launch();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ contraction -----------
-// Slot += Z_I^T W for the 64-row panel starting at row0, where consumer warp `warp` holds
-// W[row0 + warp*8 + lane/4, lt*8 + 2*(lane%4) + e] in acc[lt][e] (DMMA accumulator layout).
-// Each warp contracts its own 8 rows on the tensor pipe; the 8 warp partials of each chunk of
-// LG output tiles are summed through shared memory in warp order 0..7 (fixed order), and the
-// sum is added to the CTA-private slot (written on the CTA's first segment).
+// Slot += Z_I^T W for the 64-row panel starting at row0.  Warp (rg, ch) holds, in DMMA
+// accumulator layout, W[row0 + rg*8 + lane/4, (ch*NTW + t)*8 + 2*(lane%4) + e] in acc[t][e]
+// for its NTW local n-tiles t.  Each warp contracts its own 8 rows on the tensor pipe; the 8
+// row-group partials of every output entry are summed through shared memory in row-group order
+// 0..7 (fixed order => reproducible bits), and the sum is added to the CTA-private slot (written
+// on the CTA's first segment).  One chunk = output tile-row kt x LG local tiles of both halves
+// = NCH*LG*64 = 512 entries, one per thread.
 template <int NT>
-__device__ __forceinline__ void contract_panel(double (&acc)[NT][2], int64_t row0,
+__device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], int64_t row0,
                                                const double* __restrict__ Zp, double* red,
-                                               double* __restrict__ slot, bool first, int warp,
+                                               double* __restrict__ slot, bool first, int rg, int ch,
                                                int lane, int ctid) {
   constexpr int NP = NT * 8;
+  constexpr int NTW = (NT + 1) / 2;
+  static_assert(NCH * LG * 64 == NCW * 32, "one chunk entry per thread");
   // 1. Re-distribute W from accumulator layout to B-operand layout (rows = i, cols = l):
-  //    wb[lt][h] = W[warp*8 + 4h + lane%4, lt*8 + lane/4].
-  double wb[NT][2];
+  //    wb[t][h] = W[rg*8 + 4h + lane%4, (ch*NTW + t)*8 + lane/4].
+  double wb[NTW][2];
   const int e_sel = (lane >> 2) & 1;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int src = 16 * h + 4 * (lane & 3) + (lane >> 3);
 #pragma unroll
-    for (int lt = 0; lt < NT; ++lt) {
-      const double v0 = __shfl_sync(0xffffffffu, acc[lt][0], src);
-      const double v1 = __shfl_sync(0xffffffffu, acc[lt][1], src);
-      wb[lt][h] = e_sel ? v1 : v0;
+    for (int t = 0; t < NTW; ++t) {
+      const double v0 = __shfl_sync(0xffffffffu, acc[t][0], src);
+      const double v1 = __shfl_sync(0xffffffffu, acc[t][1], src);
+      wb[t][h] = e_sel ? v1 : v0;
     }
   }
-  // 2. A-operand rows = k, cols = i: Z[row0 + warp*8 + 4h + lane%4, kt*8 + lane/4].
-  const int64_t r0 = row0 + warp * 8 + (lane & 3);
-  const int64_t r1 = r0 + 4;
-  const double* z0 = Zp + ((r0 / BK) * NP + (lane >> 2)) * ZS + (r0 % BK);
-  const double* z1 = Zp + ((r1 / BK) * NP + (lane >> 2)) * ZS + (r1 % BK);
-  constexpr int NG = (NT + LG - 1) / LG;
+  // 2. A operand (rows = k, cols = i): Z[row0 + rg*8 + 4h + lane%4, kt*8 + lane/4], which in the
+  //    fragment-ordered Zp is lane `lane` of fragment (block r/BK, n-tile kt, k-step (r%BK)/4).
+  const int64_t r0 = row0 + rg * 8, r1 = r0 + 4;
+  const double* z0 = Zp + (((r0 / BK) * NT) * 4 + (r0 % BK) / 4) * FRAG + lane;
+  const double* z1 = Zp + (((r1 / BK) * NT) * 4 + (r1 % BK) / 4) * FRAG + lane;
+  constexpr int NG = (NTW + LG - 1) / LG;
+  // this thread's entry of every chunk
+  const int vch = ctid >> 8, vj = (ctid >> 6) & (LG - 1), v64 = ctid & 63;
+  const int vt = v64 >> 1, ve = v64 & 1;
 #pragma unroll 1
   for (int kt = 0; kt < NT; ++kt) {
-    const double za0 = z0[kt * 8 * ZS];
-    const double za1 = z1[kt * 8 * ZS];
+    const double za0 = z0[kt * 4 * FRAG];
+    const double za1 = z1[kt * 4 * FRAG];
 #pragma unroll
     for (int lg = 0; lg < NG; ++lg) {
 #pragma unroll
       for (int j = 0; j < LG; ++j) {
-        const int lt = lg * LG + j;
-        if (lt < NT) {
+        const int t = lg * LG + j;
+        if (t < NTW && ch * NTW + t < NT) {
           double o[2] = {0.0, 0.0};
-          dmma(o, za0, wb[lt][0]);
-          dmma(o, za1, wb[lt][1]);
-          *reinterpret_cast<double2*>(red + (warp * LG + j) * 64 + lane * 2) = make_double2(o[0], o[1]);
+          dmma(o, za0, wb[t][0]);
+          dmma(o, za1, wb[t][1]);
+          *reinterpret_cast<double2*>(red + ((ch * NRG + rg) * LG + j) * 64 + lane * 2) =
+              make_double2(o[0], o[1]);
         }
       }
-      // this thread's output entry of the chunk (LG*64 == NCW*32: exactly one per thread);
-      // its previous slot value is fetched before the barrier so the L2 latency overlaps it
-      static_assert(LG * 64 == NCW * 32, "one chunk entry per consumer thread");
-      const int v = ctid;
-      const int j = v >> 6;
-      const int lt = lg * LG + j;
-      const int t = (v & 63) >> 1, e = v & 1;
-      double* p = slot + (int64_t)(lt * 8 + 2 * (t & 3) + e) * NP + kt * 8 + (t >> 2);
-      const double prev = (!first && lt < NT) ? *p : 0.0;
-      named_bar_sync(1, NCW * 32);
-      if (lt < NT) {
-        double s = red[j * 64 + (v & 63)];
+      const int tl = lg * LG + vj;
+      const int lt = vch * NTW + tl;
+      const bool valid = tl < NTW && lt < NT;
+      double* p = slot + (int64_t)(lt * 8 + 2 * (vt & 3) + ve) * NP + kt * 8 + (vt >> 2);
+      const double prev = (!first && valid) ? *p : 0.0;  // L2 latency overlaps the barrier
+      __syncthreads();
+      if (valid) {
+        const double* rr = red + (vch * NRG * LG + vj) * 64 + v64;
+        double s = rr[0];
 #pragma unroll
-        for (int w = 1; w < NCW; ++w) s += red[(w * LG + j) * 64 + (v & 63)];
+        for (int g = 1; g < NRG; ++g) s += rr[g * LG * 64];
         *p = first ? s : (prev + s);
       }
-      named_bar_sync(1, NCW * 32);
+      __syncthreads();
     }
   }
 }
 
 // ------------------------------------------------------------------ K1 --------------------
-// Fill ring slot `s` with unit u = (panel I, k-block kb): BK columns of A (rows I*BM..+BM, one
-// 512 B bulk copy per column into a padded smem column) and the packed Z block kb (one bulk
-// copy).  Executed by all 32 lanes of warp 0.
-// Ragged tiles (last panel / last k-block when m is not a multiple of BM / BK): only the valid
-// rows and columns are copied; the rest of the slot keeps finite stale data (the ring is zeroed
-// at kernel start), which only ever meets the zero rows of the packed Z (rows >= m), so it adds
-// exactly 0.  Bulk copies move multiples of 16 B, so an odd count of valid rows copies one row
-// fewer and the last row is loaded with plain loads.  When A's columns are not 16-byte aligned
-// (odd lda or an 8-byte aligned A) every tile is loaded with plain loads (correct, slow).
+// Fill ring slot `s` with unit u = (panel I, k-block kb): the A tile A[I*BM.., kb*BK..] (64 x 16,
+// column-major in smem, 8 KiB) and the packed Z block kb (NT KiB).  Executed by warp 0's lanes.
+// With a tensor map (A 16-byte aligned, lda even) both are single async requests and ragged
+// tiles need nothing special: TMA zero-fills rows/columns >= m.  Otherwise the A tile is loaded
+// with plain loads and zero fill (correct, slow).
 template <int NT>
-__device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, const double* __restrict__ A,
-                                            int64_t lda, const double* __restrict__ Zp, double* As,
-                                            uint64_t* bar, int lane, uint64_t pol_a, uint64_t pol_z,
-                                            bool bulk_ok) {
-  constexpr int NP = NT * 8;
-  constexpr uint32_t zbytes = NP * ZS * 8;
+__device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, const CUtensorMap* tmap,
+                                            const double* __restrict__ A, int64_t lda,
+                                            const double* __restrict__ Zp, double* As, uint64_t* bar,
+                                            int lane, uint64_t pol_a, uint64_t pol_z, bool tma_ok) {
+  constexpr uint32_t zbytes = NT * 4 * FRAG * 8;
+  constexpr uint32_t abytes = BM * BK * 8;
   const int64_t I = u / KB, kb = u - I * KB;
   const int64_t row0 = I * BM, col0 = kb * BK;
-  double* Zs = As + BK * AS;
-  const double* zsrc = Zp + kb * (int64_t)(NP * ZS);
-  const int rows = (int)(m - row0 < BM ? m - row0 : BM);
-  const int cols = (int)(m - col0 < BK ? m - col0 : BK);
-  if (bulk_ok) {
-    const int rows_bulk = rows & ~1;
-    if (rows_bulk != rows && lane < cols)  // odd valid-row count: last row by plain loads
-      As[lane * AS + rows - 1] = A[(col0 + lane) * lda + row0 + rows - 1];
-    fence_proxy_async_smem();  // order these generic writes before later bulk writes to the slot
-    __syncwarp();
-    if (lane == 0) mbar_arrive_expect_tx(bar, zbytes + (uint32_t)(cols * rows_bulk * 8));
-    __syncwarp();
-    if (lane < cols && rows_bulk > 0)
-      bulk_g2s(As + lane * AS, A + (col0 + lane) * lda + row0, rows_bulk * 8, bar, pol_a);
-    else if (lane == BK)
+  double* Zs = As + BM * BK;
+  const double* zsrc = Zp + kb * (int64_t)(NT * 4 * FRAG);
+#ifdef OQR_EXP_NOLOAD  // experiment build only (tools/exp): no copies, barrier still completes
+  if (lane == 0) mbar_arrive(bar);
+  __syncwarp();
+  return;
+#endif
+  if (tma_ok) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(bar, abytes + zbytes);
+      tma_g2s_2d(As, tmap, (int)row0, (int)col0, bar, pol_a);
       bulk_g2s(Zs, zsrc, zbytes, bar, pol_z);
+    }
   } else {
     for (int e = lane; e < BK * BM; e += 32) {
       const int k = e / BM, r = e - k * BM;
       double v = 0.0;
-      if (r < rows && k < cols) v = A[(col0 + k) * lda + row0 + r];
-      As[k * AS + r] = v;
+      if (row0 + r < m && col0 + k < m) v = A[(col0 + k) * lda + row0 + r];
+      As[e] = v;
     }
-    fence_proxy_async_smem();
+    fence_proxy_async_smem();  // generic writes before later async-proxy writes to the slot
     __syncwarp();
     if (lane == 0) {
       mbar_arrive_expect_tx(bar, zbytes);
@@ -230,30 +249,31 @@ __device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, co
   __syncwarp();
 }
 
-// 8 warps, one CTA per SM (2 warps per SM sub-partition => up to 255 registers per thread).
-// Every warp owns 8 rows of W_I (all NP columns) in DMMA accumulators.  Warp 0 fills the ring
-// initially; afterwards whichever warp releases slot s last refills it with the unit `stages`
-// ahead, so `stages - 1` stages of compute cover the copy latency.
+// 16 warps, one CTA per SM (4 warps per SM sub-partition, <= 128 registers per thread).
+// Warp (rg = warp % 8, ch = warp / 8) owns rows rg*8..rg*8+7 of W_I and n-tiles ch*NTW..; the
+// operand fragments of k-step kk+1 are loaded while the DMMAs of k-step kk run.  Warp 0 fills
+// the ring initially; afterwards whichever warp releases slot s last refills it with the unit
+// `stages` ahead, so `stages - 1` stages of compute cover the copy latency.
 template <int NT>
 __global__ void __launch_bounds__(NCW * 32, 1)
-gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const double* __restrict__ Zp,
-                  double* __restrict__ P, int64_t KB, int64_t U, int stages, bool bulk_ok) {
+gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, const double* __restrict__ A,
+                  int64_t lda, const double* __restrict__ Zp, double* __restrict__ P, int64_t KB,
+                  int64_t U, int stages, bool tma_ok) {
   constexpr int NP = NT * 8;
-  constexpr int STAGE = BK * AS + NP * ZS;  // doubles per pipeline stage
-  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NTW = (NT + 1) / 2;
+  constexpr int STAGE = BM * BK + NT * 4 * FRAG;  // doubles per pipeline stage
+  extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
   unsigned* relcnt = reinterpret_cast<unsigned*>(empty + 8);  // 8 release counters (32 B)
-  double* red = reinterpret_cast<double*>(smem + 192);
-  double* ring = red + NCW * LG * 64;
+  double* red = reinterpret_cast<double*>(smem + 256);
+  double* ring = red + NCH * NRG * LG * 64;  // 128-byte aligned (TMA destination)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = warp % NRG, ch = warp / NRG;
   const int64_t g = gridDim.x, c = blockIdx.x;
   const int64_t u0 = U * c / g, u1 = U * (c + 1) / g;
 
-  // zero the ring once: slots of ragged tiles keep finite data outside their valid region
-  for (int e = threadIdx.x; e < stages * STAGE; e += blockDim.x) ring[e] = 0.0;
-  fence_proxy_async_smem();  // generic zero-fill before the async-proxy (bulk) writes
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
@@ -261,6 +281,7 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
       relcnt[s] = 0u;
     }
     mbar_fence_init();
+    if (tma_ok) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   __syncthreads();
 
@@ -268,35 +289,51 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
   const uint64_t pol_z = policy_evict_last();   // Zp is re-read by every panel
   if (warp == 0) {
     for (int s = 0; s < stages && u0 + s < u1; ++s)
-      issue_stage<NT>(u0 + s, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, bulk_ok);
+      issue_stage<NT>(u0 + s, KB, m, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
+                      tma_ok);
   }
 
   double* slot = P + c * (int64_t)NP * NP;
-  double acc[NT][2];
+  double acc[NTW][2];
 #pragma unroll
-  for (int lt = 0; lt < NT; ++lt) acc[lt][0] = acc[lt][1] = 0.0;
+  for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int nt_mine = (ch == 0) ? NTW : NT - NTW;  // the second half has one tile less if NT is odd
   bool first = true;
   int s = 0;
   uint32_t ph = 0;
-  const int a_off = (lane & 3) * AS + warp * 8 + (lane >> 2);
-  const int b_off = (lane >> 2) * ZS + (lane & 3);
+  // A fragment: A[row0 + rg*8 + lane/4, col0 + kk*4 + lane%4] from the column-major 64 x 16 tile
+  const int a_off = (lane & 3) * BM + rg * 8 + (lane >> 2);
+  // B fragment (lt, kk): 32 consecutive doubles of the packed block
+  const int b_off = ch * NTW * 4 * FRAG + lane;
   for (int64_t u = u0; u < u1; ++u) {
     mbar_wait(&full[s], ph);
     const double* As = ring + s * STAGE;
-    const double* Zs = As + BK * AS;
+    const double* Zs = As + BM * BK + b_off;
+    double a_cur = As[a_off];
+    double b_cur[NTW];
+#pragma unroll
+    for (int t = 0; t < NTW; ++t) b_cur[t] = (t < nt_mine) ? Zs[t * 4 * FRAG] : 0.0;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      const double a = As[kk * 4 * AS + a_off];
+      double a_nxt = 0.0, b_nxt[NTW];
+      if (kk + 1 < BK / 4) {
+        a_nxt = As[(kk + 1) * 4 * BM + a_off];
 #pragma unroll
-      for (int lt = 0; lt < NT; ++lt) {
-        const double b = Zs[lt * 8 * ZS + kk * 4 + b_off];
-        dmma(acc[lt], a, b);
+        for (int t = 0; t < NTW; ++t) b_nxt[t] = (t < nt_mine) ? Zs[(t * 4 + kk + 1) * FRAG] : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < NTW; ++t)
+        if (t < nt_mine) dmma(acc[t], a_cur, b_cur[t]);
+      if (kk + 1 < BK / 4) {
+        a_cur = a_nxt;
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) b_cur[t] = b_nxt[t];
       }
     }
     __syncwarp();
     // release the slot; the LAST warp to release it refills it at once (no warp is paced by
     // another's compute).  The arrival counter only elects that warp; the empty mbarrier's
-    // acquire then orders all eight warps' reads of the slot before the new bulk writes.
+    // acquire then orders all warps' reads of the slot before the new async writes.
     int last = 0;
     if (lane == 0) {
       mbar_arrive(&empty[s]);
@@ -305,7 +342,8 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last && u + stages < u1) {
       mbar_wait(&empty[s], ph);
-      issue_stage<NT>(u + stages, KB, m, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, bulk_ok);
+      issue_stage<NT>(u + stages, KB, m, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a,
+                      pol_z, tma_ok);
     }
     if (++s == stages) {
       s = 0;
@@ -313,10 +351,10 @@ gram_fused_kernel(int64_t m, const double* __restrict__ A, int64_t lda, const do
     }
     const int64_t I = u / KB;
     if (u + 1 == u1 || (u + 1) / KB != I) {
-      contract_panel<NT>(acc, I * BM, Zp, red, slot, first, warp, lane, threadIdx.x);
+      contract_panel<NT>(acc, I * BM, Zp, red, slot, first, rg, ch, lane, threadIdx.x);
       first = false;
 #pragma unroll
-      for (int lt = 0; lt < NT; ++lt) acc[lt][0] = acc[lt][1] = 0.0;
+      for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
     }
   }
 }
@@ -328,22 +366,28 @@ template <int NT>
 __global__ void __launch_bounds__(NCW * 32, 1)
 gram_euclid_kernel(const double* __restrict__ Zp, int64_t npanels, double* __restrict__ P) {
   constexpr int NP = NT * 8;
-  __shared__ __align__(16) double red[NCW * LG * 64];
+  constexpr int NTW = (NT + 1) / 2;
+  __shared__ __align__(16) double red[NCH * NRG * LG * 64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = warp % NRG, ch = warp / NRG;
   const int64_t g = gridDim.x, c = blockIdx.x;
   const int64_t p0 = npanels * c / g, p1 = npanels * (c + 1) / g;
   double* slot = P + c * (int64_t)NP * NP;
   bool first = true;
+  // acc[t][e] = Z[r, l] with r = I*BM + rg*8 + lane/4, l = (ch*NTW + t)*8 + 2*(lane%4) + e, i.e.
+  // lane (l%8)*4 + r%4 of fragment (r/BK, l/8, (r%BK)/4)
+  const int ln0 = (2 * (lane & 3)) * 4 + ((lane >> 2) & 3);
   for (int64_t I = p0; I < p1; ++I) {
-    const int64_t r = I * BM + warp * 8 + (lane >> 2);
-    const double* zr = Zp + ((r / BK) * NP + 2 * (lane & 3)) * ZS + (r % BK);
-    double acc[NT][2];
+    const int64_t r = I * BM + rg * 8 + (lane >> 2);
+    const double* zr = Zp + (((r / BK) * NT + ch * NTW) * 4 + (r % BK) / 4) * FRAG + ln0;
+    double acc[NTW][2];
 #pragma unroll
-    for (int lt = 0; lt < NT; ++lt) {
-      acc[lt][0] = zr[(lt * 8) * ZS];
-      acc[lt][1] = zr[(lt * 8 + 1) * ZS];
+    for (int t = 0; t < NTW; ++t) {
+      const bool ok = ch * NTW + t < NT;
+      acc[t][0] = ok ? zr[t * 4 * FRAG] : 0.0;
+      acc[t][1] = ok ? zr[t * 4 * FRAG + 4] : 0.0;
     }
-    contract_panel<NT>(acc, I * BM, Zp, red, slot, first, warp, lane, threadIdx.x);
+    contract_panel<NT>(acc, I * BM, Zp, red, slot, first, rg, ch, lane, threadIdx.x);
     first = false;
   }
 }
@@ -386,12 +430,44 @@ size_t slots_doubles(int n, int g) {
 }
 
 static int fused_stages(int NT, size_t* bytes) {
-  const size_t stage = (size_t)(BK * AS + NT * 8 * ZS) * 8;
-  const size_t fixed = 192 + (size_t)NCW * LG * 64 * 8;
+  const size_t stage = (size_t)(BM * BK + NT * 4 * FRAG) * 8;
+  const size_t fixed = 256 + (size_t)NCH * NRG * LG * 64 * 8;
   int st = (int)((SMEM_MAX - fixed) / stage);
   if (st > 8) st = 8;
   *bytes = fixed + st * stage;
   return st;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// A as a 2-D FP64 tensor {rows m (contiguous), cols m (stride lda)}, box {BM, BK}, no swizzle,
+// out-of-bounds elements zero-filled.
+static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t m, int64_t lda) {
+  if ((reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0 || m > (int64_t)INT32_MAX) return false;
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)m};
+  const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)BK};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int NT>
@@ -410,9 +486,11 @@ static cudaError_t gram_fused_nt(int64_t m, const double* A, int64_t lda, const 
   int64_t g = num_sms();
   if (g > U) g = U;
   *g_out = (int)g;
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  const bool tma_ok = make_tmap_a(&tmap, A, m, lda);
   timing_begin(s);
-  const bool bulk_ok = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
-  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(m, A, lda, Zp, P, KB, U, stages, bulk_ok);
+  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, A, lda, Zp, P, KB, U, stages, tma_ok);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);

@@ -12,24 +12,27 @@
 namespace oqr {
 
 // ---- Tiling of the fused Gram kernel (K1) and its packed Z layout ----------
-constexpr int BM = 64;        // rows of A (and of W = AZ) per panel: 8 consumer warps x 8 rows
+constexpr int BM = 64;        // rows of A (and of W = AZ) per panel: NRG row groups x 8 rows
 constexpr int BK = 16;        // columns of A (k of AZ) per pipeline stage
-constexpr int AS = BM + 4;    // smem stride (doubles) of one staged A column: with 64-bit
-                              // fragment loads, 4*k + r covers 16 distinct 8-byte banks
-constexpr int ZS = BK + 4;    // stride (doubles) of one column of a packed Z block (same rule)
-constexpr int NCW = 8;        // consumer (DMMA) warps per CTA
-constexpr int LG = 4;         // n-tiles per contraction chunk (cross-warp reduction granule)
+constexpr int NRG = 8;        // row groups per panel: 8 rows each (BM = 8 * NRG)
+constexpr int NCH = 2;        // column halves: warp (rg, ch) owns rows rg*8.. and half the n-tiles
+constexpr int NCW = NRG * NCH;  // 16 DMMA warps per CTA (4 per SM sub-partition)
+constexpr int LG = 4;         // n-tiles per warp per contraction chunk (reduction granule)
 constexpr int NTMAX = 30;     // n <= 8 * NTMAX = 240 = OQR_NMAX
 constexpr int SMEM_MAX = 227 * 1024;
+constexpr int FRAG = 32;      // doubles per DMMA operand fragment (one per lane)
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Packed Z ("Zp"): block b holds rows [b*BK, b*BK+BK) of Z as NP columns of ZS doubles,
-//   Zp[(b*NP + l)*ZS + kk] = Z[b*BK + kk, l]   (zero for kk >= BK, rows >= m, l >= n),
-// so one pipeline stage's Z tile is a single contiguous bulk copy, already in the padded,
-// bank-conflict-free smem layout.  Blocks cover every panel row: nblk = ceil(m/BM)*BM/BK.
+// Packed Z ("Zp") in DMMA B-fragment order, no padding.  Block b holds rows [b*BK, b*BK+BK)
+// of Z; inside it, fragment (lt, kk) (n-tile lt = 8 columns, k-step kk = 4 rows) is 32
+// consecutive doubles, lane-indexed as the B operand of mma.m8n8k4 wants them:
+//   Zp[((b*NT + lt)*4 + kk)*32 + lane] = Z[b*BK + kk*4 + lane%4, lt*8 + lane/4]
+// (zero for rows >= m and columns >= n).  One pipeline stage's Z tile is then one contiguous
+// bulk copy of NT KiB, and every warp fragment load is 256 consecutive bytes (conflict-free).
+// Blocks cover every panel row: nblk = ceil(m/BM)*BM/BK.
 inline int64_t zp_blocks(int64_t m) { return cdiv(m, BM) * (BM / BK); }
-inline int64_t zp_doubles(int64_t m, int NP) { return zp_blocks(m) * NP * ZS; }
+inline int64_t zp_doubles(int64_t m, int NP) { return zp_blocks(m) * (NP / 8) * 4 * FRAG; }
 
 // ---- launch bookkeeping (oqr_abi.cu) ----
 void note_launch();
@@ -40,6 +43,8 @@ void timing_end(cudaStream_t s);
 // Z (m x n, ldz) -> Zp (packed, NP = 8*ceil(n/8) columns)
 cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s);
 // Per-CTA partial Gram slots P[g][NP][NP] of Z^T (A Z); returns the grid size used in *g_out.
+// A is moved by 2-D tensor TMA when it is 16-byte aligned with an even lda; otherwise by plain
+// loads (same results, slow).
 cudaError_t launch_gram_fused(int64_t m, int n, const double* A, int64_t lda, const double* Zp,
                               double* P, int* g_out, cudaStream_t s);
 // Per-CTA partial slots of Z^T Z.

@@ -1,0 +1,27 @@
+"""Time the fused Gram kernel K1 (liboqr timing hook, CUDA events on the launching stream).
+
+    [OQR_LIB=...] python tools/time_k1.py m n [reps]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import paper_1401_5171_b200 as oqr  # noqa: E402
+
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 19968
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+p = gen.problem(m, n, 1e3, 1e2, 1234, with_A=False)
+A = torch.randn(m, m, dtype=torch.float64, device="cuda")   # timing only: values irrelevant
+Z = torch.from_numpy(p.Z).cuda()
+oqr.gram(A, Z)
+torch.cuda.synchronize()
+oqr.timing_enable(True)
+oqr.timing_reset()
+for _ in range(reps):
+    oqr.gram(A, Z)
+ms, k, tot = oqr.timing_read()
+print(f"{os.path.basename(oqr.LIB_PATH)} m={m} n={n}: K1 {ms / k:.3f} ms  {2.0 * m * m * n / (ms / k) / 1e9:.1f} TF/s")
