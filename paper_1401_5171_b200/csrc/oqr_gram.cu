@@ -205,20 +205,19 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
 }
 
 // ------------------------------------------------------------------ K1 --------------------
-// Fill ring slot `s` with unit u = (panel I, k-block kb): the A tile A[I*BM.., kb*BK..] (64 x 16,
+// Fill a ring slot with unit (panel I, k-block kb): the A tile A[I*BM.., kb*BK..] (64 x 16,
 // column-major in smem, 8 KiB) and the packed Z block kb (NT KiB).  Executed by warp 0's lanes.
 // With a tensor map (A 16-byte aligned, lda even) both are single async requests and ragged
 // tiles need nothing special: TMA zero-fills rows/columns >= m.  Otherwise the A tile is loaded
 // with plain loads and zero fill (correct, slow).
 template <int NT>
-__device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, const CUtensorMap* tmap,
+__device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, const CUtensorMap* tmap,
                                             const double* __restrict__ A, int64_t lda,
                                             const double* __restrict__ Zp, double* As, uint64_t* bar,
                                             int lane, uint64_t pol_a, uint64_t pol_z, bool tma_ok) {
   constexpr uint32_t zbytes = NT * 4 * FRAG * 8;
   constexpr uint32_t abytes = BM * BK * 8;
-  const int64_t I = u / KB, kb = u - I * KB;
-  const int64_t row0 = I * BM, col0 = kb * BK;
+  const int64_t row0 = (int64_t)I * BM, col0 = (int64_t)kb * BK;
   double* Zs = As + BM * BK;
   const double* zsrc = Zp + kb * (int64_t)(NT * 4 * FRAG);
 #ifdef OQR_EXP_NOLOAD  // experiment build only (tools/exp): no copies, barrier still completes
@@ -249,6 +248,94 @@ __device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, co
   __syncwarp();
 }
 
+// The DMMA loop of one warp over its unit range.  NTL (compile time) = this warp's n-tiles:
+// NTW for the first column half, NT - NTW for the second (one less when NT is odd), so no
+// DMMA is predicated.  Unit bookkeeping is incremental int32 (no division in the loop):
+// (I, kb) is the unit being consumed, (Ii, kbi) the unit `stages` ahead that a refill loads.
+template <int NT, int NTL>
+__device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m, const double* __restrict__ A,
+                                              int64_t lda, const double* __restrict__ Zp, double* slot,
+                                              double* red, double* ring, uint64_t* full, uint64_t* empty,
+                                              unsigned* relcnt, int KB, int u0, int u1, int stages,
+                                              bool tma_ok, int rg, int ch, int lane, uint64_t pol_a,
+                                              uint64_t pol_z) {
+  constexpr int NTW = (NT + 1) / 2;
+  constexpr int STAGE = BM * BK + NT * 4 * FRAG;
+  static_assert(NTL <= NTW, "tile split");
+  double acc[NTW][2];
+#pragma unroll
+  for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
+  bool first = true;
+  int s = 0;
+  uint32_t ph = 0;
+  int I = u0 / KB, kb = u0 - I * KB;
+  int ui = u0 + stages;  // next unit to be loaded into the slot being released
+  int Ii = ui / KB, kbi = ui - Ii * KB;
+  // A fragment: A[row0 + rg*8 + lane/4, col0 + kk*4 + lane%4] from the column-major 64 x 16 tile
+  const int a_off = (lane & 3) * BM + rg * 8 + (lane >> 2);
+  // B fragment (lt, kk): 32 consecutive doubles of the packed block
+  const int b_off = BM * BK + ch * NTW * 4 * FRAG + lane;
+  for (int u = u0; u < u1; ++u) {
+    mbar_wait(&full[s], ph);
+    const double* As = ring + s * STAGE;
+    const double* Zs = As + b_off;
+    double a_cur = As[a_off];
+    double b_cur[NTL > 0 ? NTL : 1];
+#pragma unroll
+    for (int t = 0; t < NTL; ++t) b_cur[t] = Zs[t * 4 * FRAG];
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a_nxt = 0.0, b_nxt[NTL > 0 ? NTL : 1];
+      if (kk + 1 < BK / 4) {
+        a_nxt = As[(kk + 1) * 4 * BM + a_off];
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) b_nxt[t] = Zs[(t * 4 + kk + 1) * FRAG];
+      }
+#pragma unroll
+      for (int t = 0; t < NTL; ++t) dmma(acc[t], a_cur, b_cur[t]);
+      if (kk + 1 < BK / 4) {
+        a_cur = a_nxt;
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) b_cur[t] = b_nxt[t];
+      }
+    }
+    __syncwarp();
+    // release the slot; the LAST warp to release it refills it at once (no warp is paced by
+    // another's compute).  The arrival counter only elects that warp; the empty mbarrier's
+    // acquire then orders all warps' reads of the slot before the new async writes.
+    int last = 0;
+    if (lane == 0) {
+      mbar_arrive(&empty[s]);
+      last = (atomicAdd(&relcnt[s], 1u) % NCW) == NCW - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && ui < u1) {
+      mbar_wait(&empty[s], ph);
+      issue_stage<NT>(Ii, kbi, m, tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, tma_ok);
+    }
+    ++ui;
+    if (++kbi == KB) {
+      kbi = 0;
+      ++Ii;
+    }
+    if (++s == stages) {
+      s = 0;
+      ph ^= 1;
+    }
+    const bool panel_end = (++kb == KB);
+    if (panel_end || u + 1 == u1) {
+      contract_panel<NT>(acc, (int64_t)I * BM, Zp, red, slot, first, rg, ch, lane, threadIdx.x);
+      first = false;
+#pragma unroll
+      for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
+    }
+    if (panel_end) {
+      kb = 0;
+      ++I;
+    }
+  }
+}
+
 // 16 warps, one CTA per SM (4 warps per SM sub-partition, <= 128 registers per thread).
 // Warp (rg = warp % 8, ch = warp / 8) owns rows rg*8..rg*8+7 of W_I and n-tiles ch*NTW..; the
 // operand fragments of k-step kk+1 are loaded while the DMMAs of k-step kk run.  Warp 0 fills
@@ -257,8 +344,8 @@ __device__ __forceinline__ void issue_stage(int64_t u, int64_t KB, int64_t m, co
 template <int NT>
 __global__ void __launch_bounds__(NCW * 32, 1)
 gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, const double* __restrict__ A,
-                  int64_t lda, const double* __restrict__ Zp, double* __restrict__ P, int64_t KB,
-                  int64_t U, int stages, bool tma_ok) {
+                  int64_t lda, const double* __restrict__ Zp, double* __restrict__ P, int KB,
+                  int U, int stages, bool tma_ok) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
   constexpr int STAGE = BM * BK + NT * 4 * FRAG;  // doubles per pipeline stage
@@ -271,8 +358,8 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, const dou
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rg = warp % NRG, ch = warp / NRG;
-  const int64_t g = gridDim.x, c = blockIdx.x;
-  const int64_t u0 = U * c / g, u1 = U * (c + 1) / g;
+  const int g = gridDim.x, c = blockIdx.x;
+  const int u0 = (int)((int64_t)U * c / g), u1 = (int)((int64_t)U * (c + 1) / g);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -288,75 +375,19 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, const dou
   const uint64_t pol_a = policy_evict_first();  // A is streamed exactly once
   const uint64_t pol_z = policy_evict_last();   // Zp is re-read by every panel
   if (warp == 0) {
-    for (int s = 0; s < stages && u0 + s < u1; ++s)
-      issue_stage<NT>(u0 + s, KB, m, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
+    for (int s = 0; s < stages && u0 + s < u1; ++s) {
+      const int u = u0 + s, I = u / KB;
+      issue_stage<NT>(I, u - I * KB, m, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
                       tma_ok);
+    }
   }
-
   double* slot = P + c * (int64_t)NP * NP;
-  double acc[NTW][2];
-#pragma unroll
-  for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
-  const int nt_mine = (ch == 0) ? NTW : NT - NTW;  // the second half has one tile less if NT is odd
-  bool first = true;
-  int s = 0;
-  uint32_t ph = 0;
-  // A fragment: A[row0 + rg*8 + lane/4, col0 + kk*4 + lane%4] from the column-major 64 x 16 tile
-  const int a_off = (lane & 3) * BM + rg * 8 + (lane >> 2);
-  // B fragment (lt, kk): 32 consecutive doubles of the packed block
-  const int b_off = ch * NTW * 4 * FRAG + lane;
-  for (int64_t u = u0; u < u1; ++u) {
-    mbar_wait(&full[s], ph);
-    const double* As = ring + s * STAGE;
-    const double* Zs = As + BM * BK + b_off;
-    double a_cur = As[a_off];
-    double b_cur[NTW];
-#pragma unroll
-    for (int t = 0; t < NTW; ++t) b_cur[t] = (t < nt_mine) ? Zs[t * 4 * FRAG] : 0.0;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double a_nxt = 0.0, b_nxt[NTW];
-      if (kk + 1 < BK / 4) {
-        a_nxt = As[(kk + 1) * 4 * BM + a_off];
-#pragma unroll
-        for (int t = 0; t < NTW; ++t) b_nxt[t] = (t < nt_mine) ? Zs[(t * 4 + kk + 1) * FRAG] : 0.0;
-      }
-#pragma unroll
-      for (int t = 0; t < NTW; ++t)
-        if (t < nt_mine) dmma(acc[t], a_cur, b_cur[t]);
-      if (kk + 1 < BK / 4) {
-        a_cur = a_nxt;
-#pragma unroll
-        for (int t = 0; t < NTW; ++t) b_cur[t] = b_nxt[t];
-      }
-    }
-    __syncwarp();
-    // release the slot; the LAST warp to release it refills it at once (no warp is paced by
-    // another's compute).  The arrival counter only elects that warp; the empty mbarrier's
-    // acquire then orders all warps' reads of the slot before the new async writes.
-    int last = 0;
-    if (lane == 0) {
-      mbar_arrive(&empty[s]);
-      last = (atomicAdd(&relcnt[s], 1u) % NCW) == NCW - 1;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && u + stages < u1) {
-      mbar_wait(&empty[s], ph);
-      issue_stage<NT>(u + stages, KB, m, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a,
-                      pol_z, tma_ok);
-    }
-    if (++s == stages) {
-      s = 0;
-      ph ^= 1;
-    }
-    const int64_t I = u / KB;
-    if (u + 1 == u1 || (u + 1) / KB != I) {
-      contract_panel<NT>(acc, I * BM, Zp, red, slot, first, rg, ch, lane, threadIdx.x);
-      first = false;
-#pragma unroll
-      for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
-    }
-  }
+  if (ch == 0)
+    consume_units<NT, NTW>(&tmap, m, A, lda, Zp, slot, red, ring, full, empty, relcnt, KB, u0, u1, stages,
+                           tma_ok, rg, ch, lane, pol_a, pol_z);
+  else
+    consume_units<NT, NT - NTW>(&tmap, m, A, lda, Zp, slot, red, ring, full, empty, relcnt, KB, u0, u1,
+                                stages, tma_ok, rg, ch, lane, pol_a, pol_z);
 }
 
 // ------------------------------------------------------------------ K4 --------------------
@@ -482,7 +513,8 @@ static cudaError_t gram_fused_nt(int64_t m, const double* A, int64_t lda, const 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int64_t KB = cdiv(m, BK), U = cdiv(m, BM) * KB;
+  const int64_t KB = cdiv(m, BK), U = cdiv(m, BM) * KB;  // U < 2^31 for every m that fits in HBM
+  if (U > (int64_t)INT32_MAX - 64) return cudaErrorInvalidValue;
   int64_t g = num_sms();
   if (g > U) g = U;
   *g_out = (int)g;
@@ -490,7 +522,8 @@ static cudaError_t gram_fused_nt(int64_t m, const double* A, int64_t lda, const 
   std::memset(&tmap, 0, sizeof(tmap));
   const bool tma_ok = make_tmap_a(&tmap, A, m, lda);
   timing_begin(s);
-  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, A, lda, Zp, P, KB, U, stages, tma_ok);
+  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, A, lda, Zp, P, (int)KB, (int)U, stages,
+                                                             tma_ok);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);

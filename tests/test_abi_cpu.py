@@ -60,7 +60,8 @@ def test_sass_uses_fp64_tensor_pipe_and_bulk_copy(L):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun", name, oqr.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "DMMA" in out            # mma.sync f64 -> FP64 tensor pipe
-    assert "UBLKCP" in out          # cp.async.bulk -> bulk-copy (TMA) engine
+    assert "UBLKCP" in out          # cp.async.bulk (packed Z block) -> bulk-copy engine
+    assert "UTMALDG" in out         # cp.async.bulk.tensor (A tile) -> tensor TMA
 
 
 @pytest.mark.parametrize("args,expect", [
