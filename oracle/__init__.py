@@ -60,6 +60,7 @@ def _load():
             "orc_dd_gram": (None, [I, I, P, I, P, I, P, P]),
             "orc_dd_resid": (None, [I, I, P, I, P, I, P, I, P, P]),
             "orc_dd_chol_resid": (None, [I, P, I, P, I, P, P]),
+            "orc_dd_orth_cols": (None, [I, I, P, P, I, P, I, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -175,6 +176,18 @@ def dd_orth_matrix(A, Q, m) -> np.ndarray:
     n = Q.shape[0]
     E = np.empty((n, n))
     _load().orc_dd_orth(m, n, _p(A), lda, _p(Q), ldq, _p(E))
+    return E.T.copy()
+
+
+def dd_orth_cols(A, Q, m, cols) -> np.ndarray:
+    """Q_S^T A Q_S - I for the column subset S = cols (double-double), dense |S| x |S|.
+    Same entries as dd_orth_matrix(A, Q, m)[S][:, S] (sampled checks at full sizes)."""
+    A, lda = _cm(A, m)
+    Q, ldq = _cm(Q, m)
+    c = np.ascontiguousarray(np.asarray(cols, dtype=np.int64))
+    ns = len(c)
+    E = np.empty((ns, ns))
+    _load().orc_dd_orth_cols(m, ns, c.ctypes.data_as(ctypes.c_void_p), _p(A), lda, _p(Q), ldq, _p(E))
     return E.T.copy()
 
 

@@ -27,6 +27,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* ------------------------------------------------------------------------- */
 /* Algorithm 1 (CHOLQR) step 1-2:  B = A Z;  C = Z^T B.      */
@@ -322,4 +325,42 @@ void orc_dd_chol_resid(int64_t n, const double* G, int64_t ldg, const double* R,
       D[l * n + k] = s.hi + s.lo;
       RRabs[l * n + k] = sa;
     }
+}
+
+/* E_S = Q_S^T A Q_S - I for the column subset S (ns columns, indices cols[]), n_s x n_s (ld ns),
+ * double-double.  Identical per-entry arithmetic to orc_dd_orth (AQ[i,l] accumulated over j
+ * ascending, then E[k,l] over i ascending); only the loop order over (i, j) is interchanged so
+ * that column-major A is streamed once (rows i are split across threads).  Used for sampled
+ * orthogonality checks at the full BASELINE sizes. */
+void orc_dd_orth_cols(int64_t m, int64_t ns, const int64_t* cols, const double* A, int64_t lda,
+                      const double* Q, int64_t ldq, double* E) {
+  dd_t* AQ = (dd_t*)malloc(sizeof(dd_t) * m * ns);
+#pragma omp parallel
+  {
+    int nt = 1, t = 0;
+#ifdef _OPENMP
+    nt = omp_get_num_threads();
+    t = omp_get_thread_num();
+#endif
+    int64_t i0 = m * t / nt, i1 = m * (t + 1) / nt;
+    for (int64_t l = 0; l < ns; l++)
+      for (int64_t i = i0; i < i1; i++) { AQ[l * m + i].hi = 0.0; AQ[l * m + i].lo = 0.0; }
+    for (int64_t j = 0; j < m; j++) {
+      const double* acol = A + j * lda;
+      for (int64_t l = 0; l < ns; l++) {
+        const double q = Q[cols[l] * ldq + j];
+        dd_t* aq = AQ + l * m;
+        for (int64_t i = i0; i < i1; i++) aq[i] = dd_add_prod(aq[i], acol[i], q);
+      }
+    }
+  }
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < ns; l++)
+    for (int64_t k = 0; k < ns; k++) {
+      dd_t s = {k == l ? -1.0 : 0.0, 0.0};
+      const double* qk = Q + cols[k] * ldq;
+      for (int64_t i = 0; i < m; i++) s = dd_add_dd_prod(s, qk[i], AQ[l * m + i]);
+      E[l * ns + k] = s.hi + s.lo;
+    }
+  free(AQ);
 }

@@ -1,0 +1,108 @@
+"""GPU parity at BASELINE.json's FULL sizes (configs[2], configs[3], configs[4] and the configs[4]
+breakdown witness), through the same C-ABI calls bench.py times (oqr_normal / oqr_normal2 /
+oqr_prequr on device-resident inputs).
+
+Checked against the CPU oracle on the same seeded inputs:
+  * T1: every entry of G = Z^T A Z within 2 gamma_{3m} (|Z|^T|A||Z|)  (eq.mult1-2)
+  * T7: outcome class (the witness must break down for normal / normal2 and not for prequr)
+  * T2: componentwise representativity on ALL of Q, R (double-double residual, O(mn^2))
+  * T5: orthogonality on a sampled column subset S (|S| = 8): Q_S^T A Q_S - I in double-double,
+        against 10 E_orc + 10 n u ||A|| ||Q_orc||^2 on the same S
+  * T6: R and Q against the oracle's, first-order perturbation tolerances (test_gpu_parity)
+  * T8: bitwise determinism of two calls
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from oracle import U, gamma
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+SAMPLE_COLS = 8
+
+
+def absA_absZ(p):
+    """M = |Z|^T |A| |Z| in FP64 (a tolerance scale, not a parity value), blockwise over A."""
+    m = p.m
+    Zd = np.abs(oracle.from_cm(p.Z, m))
+    AZ = np.zeros((m, p.n))
+    for j0 in range(0, m, 2048):
+        j1 = min(m, j0 + 2048)
+        AZ += np.abs(p.A[j0:j1, :m]).T @ Zd[j0:j1]
+    return Zd.T @ AZ
+
+
+@pytest.fixture(scope="module", params=["c4", "witness", "c2", "c3"])
+def case(request):
+    import paper_1401_5171_b200 as oqr
+    name = request.param
+    p = gen.witness() if name == "witness" else gen.config(int(name[1]))
+    A = torch.from_numpy(p.A).to(DEV)
+    Z = torch.from_numpy(p.Z).to(DEV)
+    d = dict(name=name, p=p, A=A, Z=Z, oqr=oqr, M=absA_absZ(p),
+             G=oracle.from_cm(oracle.gram(p.A, p.Z, p.m), p.n))
+    yield d
+    del d["A"], d["Z"]
+    torch.cuda.empty_cache()
+
+
+def test_t1_gram_full(case):
+    p, oqr = case["p"], case["oqr"]
+    n = p.n
+    Gg = oqr.gram(case["A"], case["Z"]).cpu().numpy().T
+    Go = case["G"]
+    tol = 2 * gamma(3 * p.m) * case["M"]
+    bad = np.abs(Gg - Go) > tol
+    assert not bad.any(), (np.argwhere(bad)[:5], (np.abs(Gg - Go) / case["M"]).max())
+
+
+def sampled_cols(n):
+    return sorted(set([0, 1, 2, 3, n // 2, n - 3, n - 2, n - 1]))[:SAMPLE_COLS]
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+def test_variants_full(case, variant):
+    p, oqr = case["p"], case["oqr"]
+    m, n = p.m, p.n
+    Q, R, st = oqr.VARIANTS[variant](case["A"], case["Z"])
+    Q2, R2, st2 = oqr.VARIANTS[variant](case["A"], case["Z"])
+    assert st == st2 and torch.equal(Q, Q2) and torch.equal(R, R2)             # T8
+    Qo, Ro, sto = oracle.VARIANTS[variant](p.A, p.Z, m)
+    cls = lambda s: 0 if s == 0 else (1 if s <= n else 2)
+    if case["name"] == "witness":                                               # T7
+        # kappa(A^{1/2}Z)^2 = kappa(G) = 1e20 >> 1/u: CHOLQR breaks down in its first Cholesky
+        # (normal2 in pass 1); the pre-QR variant's A-stage is well conditioned (s8(c) item 14)
+        expect = 0 if variant == "prequr" else 1
+        assert cls(st) == expect and cls(sto) == expect, (st, sto)
+    else:
+        assert st == 0 and sto == 0, (st, sto)
+    if st != 0:
+        return
+    Qg, Rg = Q.cpu().numpy(), R.cpu().numpy()
+    rho = oracle.componentwise_ratio(p.Z, Qg, Rg, m)                            # T2
+    if variant == "normal":
+        assert rho <= gamma(n + 1), rho / U
+    else:
+        rho_o = oracle.componentwise_ratio(p.Z, Qo, Ro, m)
+        assert rho <= 10 * rho_o + 4 * gamma(n + 1), (rho / U, rho_o / U)
+    S = sampled_cols(n)                                                          # T5 (sampled)
+    E = np.linalg.norm(oracle.dd_orth_cols(p.A, Qg, m, S), 2)
+    Eo = np.linalg.norm(oracle.dd_orth_cols(p.A, Qo, m, S), 2)
+    normQ = np.linalg.norm(oracle.from_cm(Qo, m), 2)
+    assert E <= 10 * Eo + 10 * n * U * float(np.max(p.d)) * normQ ** 2, (E, Eo)
+    # T6: first-order perturbation bounds (see test_gpu_parity.forward_tols)
+    G = case["G"]
+    Rd, Qd = oracle.from_cm(Ro, n), oracle.from_cm(Qo, m)
+    dG = np.linalg.norm(2 * gamma(3 * m) * case["M"] + 2 * gamma(n + 1) * (np.abs(Rd).T @ np.abs(Rd)))
+    sG = np.linalg.svd(G, compute_uv=False)
+    sR = np.linalg.svd(Rd, compute_uv=False)
+    tol_R = math.sqrt(2) * (sG[0] / sG[-1]) * sR[0] * dG / sG[0]
+    tol_Q = (np.linalg.norm(Qd, 2) * tol_R + 2 * gamma(n + 1) * np.linalg.norm(np.abs(Qd) @ np.abs(Rd))) / sR[-1]
+    assert np.linalg.norm(Rg - Ro) <= tol_R
+    assert np.linalg.norm(Qg - Qo) <= tol_Q

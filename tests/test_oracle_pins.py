@@ -378,3 +378,14 @@ def test_p6_variant_representativity(cfg, variant):
     X = _sqrtA_times(p, dense(p.Z, m))
     kG = np.linalg.cond(X) ** 2
     assert np.linalg.norm(dense(R, n) - dense(R0, n)) / np.linalg.norm(dense(R0, n)) <= 10 * np.sqrt(m) * U * kG
+
+
+def test_dd_orth_cols_equals_full_checker_bitwise():
+    # the sampled checker is the full checker restricted to S (same per-entry arithmetic)
+    p = gen.problem(333, 12, 1e4, 1e3, 8, lda=340)
+    Q, _, info = oracle.normal(p.A, p.Z, p.m)
+    assert info == 0
+    E = oracle.dd_orth_matrix(p.A, Q, p.m)
+    cols = [0, 3, 7, 11]
+    Es = oracle.dd_orth_cols(p.A, Q, p.m, cols)
+    assert np.array_equal(Es, E[np.ix_(cols, cols)])
