@@ -5,55 +5,113 @@ namespace oqr {
 
 // ------------------------------------------------------------------ K2 --------------------
 // R = chol(G), upper, R^T R = G: Algorithm 1 line 3, backward error
-// eq:normal:chol.  One CTA; the upper triangle of G lives packed in shared
-// memory (column-major packed index l(l+1)/2 + k, k <= l; n = 240 -> 231,360 B).  Right-looking:
-// at step j the pivot d = a_jj is tested with the LAPACK rule (breakdown iff !(d > 0), which
-// also catches NaN; reading R4), row j is scaled by 1/sqrt(d) (true division), and the
-// trailing upper triangle is updated a_kl -= r_jk r_jl.  Only the upper triangle is read.
+// eq:normal:chol.  One CTA of 1024 threads; the upper triangle of G lives
+// packed in shared memory (column-major packed index l(l+1)/2 + k, k <= l), padded to a
+// multiple of 8 with an identity block (n = 240 -> 231,360 B).  Blocked right-looking with 8x8
+// blocks -- the same operations as the unblocked algorithm in a different order:
+//   1. warp 0 factors the diagonal block: pivot d = a_pp, breakdown iff !(d > 0) (LAPACK rule,
+//      catches NaN; reading R4), r_pp = sqrt(d), row p of the block divided by r_pp,
+//      the block's trailing triangle updated;
+//   2. one thread per column l solves the block row: r_pl = (a_pl - sum_{c'<c} r_c'p r_c'l)/r_pp;
+//   3. the trailing upper triangle is updated tile by tile on the FP64 tensor pipe:
+//      A_kl -= R_{j,k}^T R_{j,l} (8x8x8 per tile, mma.m8n8k4 x 2).
+// Only the upper triangle of G is read.
 __device__ __forceinline__ int pk(int k, int l) { return l * (l + 1) / 2 + k; }
+
+__device__ __forceinline__ void dmma_c(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
 
 __global__ void __launch_bounds__(1024, 1)
 potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ R, int64_t ldr,
              int* info, int info_off) {
   extern __shared__ double S[];
+  __shared__ int s_brk;
   if (info_off > 0 && *info != 0) return;  // an earlier stage already broke down
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int l = ty; l < n; l += 32)
-    for (int k = tx; k <= l; k += 32) S[pk(k, l)] = G[(int64_t)l * ldg + k];
+  const int NT = (n + 7) / 8, NP = NT * 8;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  for (int l = warp; l < NP; l += nwarp)
+    for (int k = lane; k <= l; k += 32)
+      S[pk(k, l)] = (l < n) ? G[(int64_t)l * ldg + k] : (k == l ? 1.0 : 0.0);
+  if (tid == 0) s_brk = 0;
   __syncthreads();
-  int brk = 0;
-  for (int j = 0; j < n; ++j) {
-    const double d = S[pk(j, j)];
-    if (!(d > 0.0)) {  // uniform: every thread read the same value after the last barrier
-      brk = j + 1;
-      break;
+  for (int j = 0; j < NT; ++j) {
+    const int j0 = j * 8;
+    // 1. diagonal block (warp 0)
+    if (warp == 0) {
+      for (int c = 0; c < 8; ++c) {
+        const int p = j0 + c;
+        const double d = S[pk(p, p)];
+        if (!(d > 0.0)) {  // uniform across the warp
+          if (lane == 0) s_brk = p + 1;
+          break;
+        }
+        const double r = sqrt(d);
+        __syncwarp();
+        if (lane < 7 - c) S[pk(p, p + 1 + lane)] = S[pk(p, p + 1 + lane)] / r;
+        __syncwarp();
+        if (lane == 0) S[pk(p, p)] = r;
+        for (int e = lane; e < 64; e += 32) {
+          const int a = e >> 3, b = e & 7;
+          if (a > c && b >= a) S[pk(j0 + a, j0 + b)] -= S[pk(p, j0 + a)] * S[pk(p, j0 + b)];
+        }
+        __syncwarp();
+      }
     }
-    const double rjj = sqrt(d);
-    __syncthreads();  // all reads of a_jj done before it is overwritten
-    for (int l = j + 1 + threadIdx.x; l < n; l += blockDim.x) S[pk(j, l)] = S[pk(j, l)] / rjj;
-    if (threadIdx.x == 0) S[pk(j, j)] = rjj;
     __syncthreads();
-    for (int l = j + 1 + ty; l < n; l += 32) {
-      const double rjl = S[pk(j, l)];
-      for (int k = j + 1 + tx; k <= l; k += 32) S[pk(k, l)] -= S[pk(j, k)] * rjl;
+    if (s_brk) break;
+    // 2. block row j: columns l >= j0 + 8 (one thread each), forward substitution with R_jj^T
+    for (int l = j0 + 8 + tid; l < NP; l += blockDim.x) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int p = j0 + c;
+        double x = S[pk(p, l)];
+        for (int c2 = 0; c2 < c; ++c2) x -= S[pk(j0 + c2, p)] * S[pk(j0 + c2, l)];
+        S[pk(p, l)] = x / S[pk(p, p)];
+      }
+    }
+    __syncthreads();
+    // 3. trailing update on DMMA: tiles (kt, lt), j < kt <= lt < NT
+    const int rem = NT - j - 1;
+    const int ntiles = rem * (rem + 1) / 2;
+    for (int t = warp; t < ntiles; t += nwarp) {
+      int lt = 0;                                  // t = lt*(lt+1)/2 + kt  (local indices)
+      while ((lt + 1) * (lt + 2) / 2 <= t) ++lt;
+      const int kt = t - lt * (lt + 1) / 2;
+      const int k0 = (j + 1 + kt) * 8, l0 = (j + 1 + lt) * 8;
+      double acc[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = j0 + 4 * h + (lane & 3);
+        dmma_c(acc, S[pk(p, k0 + (lane >> 2))], S[pk(p, l0 + (lane >> 2))]);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = k0 + (lane >> 2), l = l0 + 2 * (lane & 3) + e;
+        if (k <= l) S[pk(k, l)] -= acc[e];
+      }
     }
     __syncthreads();
   }
-  if (brk) {
-    if (threadIdx.x == 0) *info = info_off + brk;
+  if (s_brk) {
+    if (tid == 0) *info = info_off + s_brk;
     return;
   }
-  for (int l = ty; l < n; l += 32)
-    for (int k = tx; k < n; k += 32) R[(int64_t)l * ldr + k] = (k <= l) ? S[pk(k, l)] : 0.0;
-  if (threadIdx.x == 0 && info_off == 0) *info = 0;
+  for (int l = warp; l < n; l += nwarp)
+    for (int k = lane; k < n; k += 32) R[(int64_t)l * ldr + k] = (k <= l) ? S[pk(k, l)] : 0.0;
+  if (tid == 0 && info_off == 0) *info = 0;
 }
 
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
                          int info_off, cudaStream_t s) {
-  const size_t bytes = (size_t)n * (n + 1) / 2 * sizeof(double);
+  const int NP = 8 * ((n + 7) / 8);
+  const size_t bytes = (size_t)NP * (NP + 1) / 2 * sizeof(double);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    cudaError_t e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_MAX - 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -65,66 +123,199 @@ cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t
 // ------------------------------------------------------------------ K3 --------------------
 // Q = Z R^{-1}: Algorithm 1 line 4 as the row-wise substitution whose backward
 // error is stated at PAPER.md:197-198:  q_ij = (z_ij - sum_{k<j} q_ik r_kj) / r_jj.
-// One thread per row (coalesced: consecutive threads = consecutive rows of column-major Z/Q).
-// Columns are processed in blocks of NB: the NB partial sums stay in registers while k runs
-// 0..j-1 in ascending order, so each q_ij is the true substitution value (no explicit R^{-1}).
-// The thread's finished q_i,0..j-1 are kept in shared memory (column-major, conflict-free),
-// the current R column block is staged in shared memory and read as a broadcast.
-constexpr int TRSM_NB = 8;
+// One warp per 8 rows; columns in tiles of 8 (jt).  For tile jt the partial sums
+// sum_{k < 8 jt} q_ik r_kj run on the FP64 tensor pipe (mma.m8n8k4, K = 8 jt), with the row's
+// finished q's kept in registers as DMMA A-fragments; then the 8 x 8 diagonal block is solved
+// by plain substitution: column c of the tile is (z - s - sum_{c'<c} q_c' r_c'c) / r_cc with the
+// running sum held in the lane that owns the entry and q_c broadcast to the row's 4 lanes.
+// This is the substitution formula with the sum split into pieces (a summation order), never an
+// explicit inverse, so the componentwise bound |dR^i| <= gamma_n |R| still holds.
+__device__ __forceinline__ void dmma_f(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
 
-__global__ void trsm_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q
-                            const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq,
-                            const int* info) {
+// R is staged once per (persistent) CTA in shared memory in DMMA B-fragment order:
+//   Rt[((jt*(jt-1)/2 + kt)*2 + h)*32 + lane] = R[kt*8 + 4h + lane%4, jt*8 + lane/4]   (kt < jt)
+//   Rd[(jt*8 + c)*8 + c2] = R[jt*8 + c, jt*8 + c2]  (diagonal tiles; 1 on the diagonal beyond n)
+// so every fragment load is 256 consecutive bytes.  NT = 30 does not fit (238 KB) and gathers
+// its fragments from global memory (L2) instead.
+constexpr int TRSM_THREADS = 256;  // 8 warps: <= 255 registers, the q fragments stay in registers
+
+template <int NT>
+constexpr size_t trsm_smem_doubles() { return (size_t)NT * (NT - 1) / 2 * 64 + (size_t)NT * 64; }
+
+template <int NT, bool SMEM_R>
+__global__ void __launch_bounds__(TRSM_THREADS, 1)
+trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q (in place)
+                 const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info) {
   if (info != nullptr && *info != 0) return;
-  extern __shared__ double sm[];
-  const int T = blockDim.x, tid = threadIdx.x;
-  double* Qs = sm;                       // [n][T]
-  double* Rb = sm + (size_t)n * T;       // [(n + NB)][NB]
-  const int64_t i = blockIdx.x * (int64_t)T + tid;
-  const bool valid = i < m;
-  for (int jb = 0; jb < n; jb += TRSM_NB) {
-    __syncthreads();
-    const int rows = jb + TRSM_NB;
-    for (int e = tid; e < rows * TRSM_NB; e += T) {
-      const int k = e / TRSM_NB, c = e - k * TRSM_NB;
-      Rb[e] = (jb + c < n && k < n) ? R[(int64_t)(jb + c) * ldr + k] : 0.0;
+  extern __shared__ __align__(16) double rsm[];
+  double* const Rt_base = rsm;
+  double* const Rd_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
+  if (SMEM_R) {
+    double* Rt = Rt_base;
+    double* Rd = Rd_base;
+    for (int jt = 1; jt < NT; ++jt) {  // tiles (kt < jt) of column tile jt: jt*64 doubles
+      double* dst = Rt + (size_t)jt * (jt - 1) / 2 * 64;
+      for (int e = threadIdx.x; e < jt * 64; e += blockDim.x) {
+        const int ln = e & 31, h = (e >> 5) & 1, kt = e >> 6;
+        const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
+        dst[e] = (col < n) ? R[(int64_t)col * ldr + k] : 0.0;
+      }
+    }
+    for (int e = threadIdx.x; e < NT * 64; e += blockDim.x) {
+      const int jt = e >> 6, c = (e >> 3) & 7, c2 = e & 7;
+      const int r = jt * 8 + c, col = jt * 8 + c2;
+      double v = 0.0;
+      if (c <= c2) v = (col < n) ? R[(int64_t)col * ldr + r] : (c == c2 ? 1.0 : 0.0);
+      Rd[e] = v;
     }
     __syncthreads();
-    double s[TRSM_NB];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int q4 = lane & 3;                // quad position: C columns 2*q4, 2*q4 + 1
+  const int gbase = lane & ~3;            // first lane of this row's quad
+#pragma unroll 1
+  for (int64_t r0 = ((int64_t)blockIdx.x * nw + warp) * 8; r0 < m; r0 += (int64_t)gridDim.x * nw * 8) {
+    const int64_t row = r0 + (lane >> 2);
+    const bool row_ok = row < m;
+    // opaque per-iteration copies of the smem bases: stops the compiler from hoisting the
+    // (loop-invariant) R fragment loads out of the row loop into hundreds of registers
+    const double* Rt = Rt_base;
+    const double* Rd = Rd_base;
+    int64_t ldz_l = ldz, ldq_l = ldq;  // likewise the per-column offsets col*ldz, col*ldq
+    int n_l = n;                       // and the per-column predicates col < n
+    asm volatile("" : "+l"(Rt), "+l"(Rd), "+l"(ldz_l), "+l"(ldq_l), "+r"(n_l));
+    double qa[NT][2];                     // A fragments: Q[r0 + lane/4, jt*8 + 4h + lane%4]
+    // Z of tile jt+1 is loaded before tile jt's Q stores: different columns, so this is safe
+    // even in place (Q == Z), and it takes the global-load latency off the per-tile chain
+    // (the compiler must assume Q aliases Z and would not reorder these itself).
+    double znext[2];
 #pragma unroll
-    for (int c = 0; c < TRSM_NB; ++c) s[c] = (valid && jb + c < n) ? Z[(int64_t)(jb + c) * ldz + i] : 0.0;
-    for (int k = 0; k < jb; ++k) {
-      const double qk = Qs[(size_t)k * T + tid];
-      const double* rk = Rb + k * TRSM_NB;
-#pragma unroll
-      for (int c = 0; c < TRSM_NB; ++c) s[c] -= qk * rk[c];
+    for (int e = 0; e < 2; ++e) {
+      const int col = 2 * q4 + e;
+      znext[e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
     }
 #pragma unroll
-    for (int c = 0; c < TRSM_NB; ++c) {
-      if (jb + c < n) {
-        const double q = s[c] / Rb[(jb + c) * TRSM_NB + c];
-        Qs[(size_t)(jb + c) * T + tid] = q;
+    for (int jt = 0; jt < NT; ++jt) {
+      const double zc0 = znext[0], zc1 = znext[1];
+      if (jt + 1 < NT) {
 #pragma unroll
-        for (int c2 = c + 1; c2 < TRSM_NB; ++c2) s[c2] -= q * Rb[(jb + c) * TRSM_NB + c2];
-        if (valid) Q[(int64_t)(jb + c) * ldq + i] = q;
+        for (int e = 0; e < 2; ++e) {
+          const int col = (jt + 1) * 8 + 2 * q4 + e;
+          znext[e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+        }
+      }
+      // off-diagonal partial sums on DMMA (two accumulators: independent chains)
+      double s0[2] = {0.0, 0.0}, s1[2] = {0.0, 0.0};
+      const int bcol = jt * 8 + (lane >> 2);
+      const double* rb = R + (int64_t)(bcol < n ? bcol : 0) * ldr + q4;
+#pragma unroll
+      for (int kt = 0; kt < jt; ++kt) {
+        double b0, b1;
+        if (SMEM_R) {
+          const double* f = Rt + (size_t)(jt * (jt - 1) / 2 + kt) * 64 + lane;
+          b0 = f[0];
+          b1 = f[32];
+        } else {
+          b0 = bcol < n ? rb[kt * 8] : 0.0;
+          b1 = bcol < n ? rb[kt * 8 + 4] : 0.0;
+        }
+        if (kt & 1) {
+          dmma_f(s1, qa[kt][0], b0);
+          dmma_f(s1, qa[kt][1], b1);
+        } else {
+          dmma_f(s0, qa[kt][0], b0);
+          dmma_f(s0, qa[kt][1], b1);
+        }
+      }
+      // t = z - s for this lane's two entries (row, jt*8 + 2*q4 + e)
+      double t[2];
+      t[0] = zc0 - (s0[0] + s1[0]);
+      t[1] = zc1 - (s0[1] + s1[1]);
+      // diagonal 8 x 8 block by substitution
+      double qc[2] = {0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int dc = jt * 8 + c;
+        double rcc;
+        if (SMEM_R) rcc = Rd[(jt * 8 + c) * 8 + c];
+        else rcc = dc < n ? R[(int64_t)dc * ldr + dc] : 1.0;
+        const double mine = t[c & 1] / rcc;  // meaningful in the owner lane (q4 == c/2)
+        const double qv = __shfl_sync(0xffffffffu, mine, gbase | (c >> 1));
+        if (q4 == (c >> 1)) qc[c & 1] = qv;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 2 * q4 + e;
+          if (col > c) {
+            const int gc = jt * 8 + col;
+            double rcj;
+            if (SMEM_R) rcj = Rd[(jt * 8 + c) * 8 + col];
+            else rcj = gc < n ? R[(int64_t)gc * ldr + dc] : 0.0;
+            t[e] -= qv * rcj;
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = jt * 8 + 2 * q4 + e;
+        if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qc[e];
+      }
+      // C layout -> A fragments of this tile: qa[jt][h] = q(row, jt*8 + 4h + lane%4)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int src = gbase | (2 * h + (q4 >> 1));
+        const double v0 = __shfl_sync(0xffffffffu, qc[0], src);
+        const double v1 = __shfl_sync(0xffffffffu, qc[1], src);
+        qa[jt][h] = (lane & 1) ? v1 : v0;
       }
     }
   }
 }
 
-cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
-                        double* Q, int64_t ldq, const int* info, cudaStream_t s) {
+static int trsm_num_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+template <int NT>
+static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
+                           double* Q, int64_t ldq, const int* info, cudaStream_t s) {
+  constexpr size_t bytes = trsm_smem_doubles<NT>() * sizeof(double);
+  constexpr bool smem_r = bytes <= (size_t)SMEM_MAX;
   static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+  if (smem_r && !attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(trsm_dmma_kernel<NT, smem_r>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const size_t rb = (size_t)(n + TRSM_NB) * TRSM_NB * sizeof(double);
-  int T = 128;
-  while (T > 32 && (size_t)n * T * sizeof(double) + rb > (size_t)SMEM_MAX) T >>= 1;
-  const size_t bytes = (size_t)n * T * sizeof(double) + rb;
-  trsm_kernel<<<(unsigned)cdiv(m, T), T, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
+  int64_t g = cdiv(m, (TRSM_THREADS / 32) * 8);  // 8 rows per warp per pass
+  const int sms = trsm_num_sms();
+  if (g > sms) g = sms;          // persistent: R is staged once per CTA
+  trsm_dmma_kernel<NT, smem_r><<<(unsigned)g, TRSM_THREADS, smem_r ? bytes : 0, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
+  return cudaSuccess;
+}
+
+#define OQR_TRSM_CASES(X) \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
+  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
+
+cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
+                        double* Q, int64_t ldq, const int* info, cudaStream_t s) {
+  cudaError_t e;
+  switch ((int)cdiv(n, 8)) {
+#define OQR_CASE(NT) \
+  case NT: e = trsm_nt<NT>(m, n, Z, ldz, R, ldr, Q, ldq, info, s); break;
+    OQR_TRSM_CASES(OQR_CASE)
+#undef OQR_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
 }

@@ -72,7 +72,9 @@ def test_variants_full(case, variant):
     m, n = p.m, p.n
     Q, R, st = oqr.VARIANTS[variant](case["A"], case["Z"])
     Q2, R2, st2 = oqr.VARIANTS[variant](case["A"], case["Z"])
-    assert st == st2 and torch.equal(Q, Q2) and torch.equal(R, R2)             # T8
+    assert st == st2                                                            # T8
+    if st == 0:                        # on breakdown Q and R are unspecified (include/oqr.h)
+        assert torch.equal(Q, Q2) and torch.equal(R, R2)
     Qo, Ro, sto = oracle.VARIANTS[variant](p.A, p.Z, m)
     cls = lambda s: 0 if s == 0 else (1 if s <= n else 2)
     if case["name"] == "witness":                                               # T7

@@ -1,0 +1,45 @@
+"""Per-step CUDA-event timings through the step exports (pack+K1+K1r, K2, K3) and the three
+variants, for one BASELINE config.      python tools/time_steps.py [config] [reps]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import paper_1401_5171_b200 as oqr  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+p = gen.config(cfg)
+m, n = p.m, p.n
+A = torch.from_numpy(p.A).cuda()
+Z = torch.from_numpy(p.Z).cuda()
+
+
+def timed(fn):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+G = oqr.gram(A, Z)
+R, info = oqr.potrf(G)
+torch.cuda.synchronize()
+assert int(info.item()) == 0
+res = {"gram (pack+K1+K1r)": timed(lambda: oqr.gram(A, Z, G)),
+       "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)),
+       "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
+for v in ("normal", "normal2", "prequr"):
+    Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    Rv = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    res[v] = timed(lambda: oqr.VARIANTS[v](A, Z, Q, Rv))
+fl = 2.0 * m * m * n + 2.0 * m * n * n
+print(f"config {cfg} m={m} n={n}: " + ", ".join(f"{k} {v:.4f} ms" for k, v in res.items()) +
+      f"; normal {fl / res['normal'] / 1e9:.1f} GFLOP/s")
