@@ -38,6 +38,7 @@ import gen  # noqa: E402
 
 FP64_DMMA_PEAK_TFLOPS = 37.2   # tools/k0_probe.cu on this pool's B200 (profiles/r01_k0_probe.txt)
 PEAK_SOURCE = "measured: K0 DMMA m8n8k4 microbenchmark, sustained, profiles/r01_k0_probe.txt"
+METRIC = "oblique-QR GFLOP/s (FP64, 1 B200) and % of FP64 roofline"
 
 
 def flops_paper(m, n):
@@ -152,7 +153,7 @@ def reference_arm(args, cfg, rank):
     v = flops_paper(r, n) / dt / 1e9
     base.update(value=v)
     line = {
-        "impl": "reference", "metric": "oblique-QR GFLOP/s (FP64)", "value": v, "unit": "GFLOP/s",
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"configs[{cfg}] oqr_{args.variant} m={m} n={n}; "
@@ -296,7 +297,7 @@ def main():
             cpu, _, _ = cpu_oracle_sample(p)
         peaks = measured_peaks()
         line = {
-            "metric": "oblique-QR GFLOP/s (FP64, 1 B200) and % of FP64 roofline",
+            "metric": METRIC,
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
