@@ -8,8 +8,9 @@ K1r, Cholesky K2, triangular solve K3) on BASELINE.json configs[3] (m = 40000, n
 12.8 GB > the 126 MB L2, so no L2 flush is needed between steps).  Prints ONE JSON line (rank 0).
 
 value    = whole-job FP64 GFLOP/s with inputs resident in HBM, the paper's normalisation
-           (2 m^2 n + 2 m n^2) / T, summed over ranks (N > 1: independent
-           replicas).
+           (2 m^2 n + 2 m n^2) / T.  N > 1 (torchrun): the same problem
+           row-sharded over the ranks (strong scaling; one n x n all-gather per step; DESIGN.md
+           s9), T = max over ranks.
 e2e      = the same metric with pinned-host A, Z copied in and Q, R copied out every step.
 roofline = the fused Gram kernel K1, timed live with CUDA events on the launching stream
            (liboqr's timing hook): achieved = 2 m^2 n flops / mean K1 launch time against the
@@ -192,6 +193,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded code path even at N = 1 (it is the default for N > 1)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("OQR_BENCH_ALLOW_SHORT"), \
         "use --warmup >= 3"
@@ -214,20 +217,38 @@ def main():
     c = gen.CONFIGS[args.config]
     m, n = c["m"], c["n"]
     fl = flops_paper(m, n)
-    fl_gram = 2.0 * m * m * n
-
-    # inputs: generated once on the host straight into pinned buffers, then copied to HBM
-    A_h = pinned((m, m))
+    stream = torch.cuda.current_stream()
     Z_h = pinned((n, m))
-    p = gen.config(args.config, A_out=A_h.numpy(), Z_out=Z_h.numpy())
+    if world == 1 and not args.sharded:
+        # inputs: generated once on the host straight into pinned buffers, then copied to HBM
+        A_h = pinned((m, m))
+        p = gen.config(args.config, A_out=A_h.numpy(), Z_out=Z_h.numpy())
+        r0, mr = 0, m
+        Q_h = pinned((n, m))
+        fn = oqr.VARIANTS[args.variant]
+        Q = torch.empty((n, m), dtype=torch.float64, device=dev)
+        R = torch.empty((n, n), dtype=torch.float64, device=dev)
+
+        def step(A, Z):
+            Qo, Ro, st = fn(A, Z, Q, R)
+            return Qo, Ro, st
+    else:
+        # row-sharded strong scaling: this rank generates and holds only its rows
+        from paper_1401_5171_b200.dist import normal_rows, row_partition
+        assert args.variant == "normal", "the row-sharded path implements oqr_normal"
+        r0, mr = row_partition(m, world)[rank]
+        ldar = mr + (mr & 1)
+        A_h = pinned((m, ldar))
+        gen.config_A_rows(args.config, r0, r0 + mr, lda=ldar, out=A_h.numpy())
+        p = gen.config(args.config, with_A=False, Z_out=Z_h.numpy())
+        Q_h = pinned((n, mr))
+
+        def step(A, Z):
+            return normal_rows(A, Z, r0, mr)
+    fl_gram = 2.0 * mr * m * n  # per K1 launch on this rank
     A = A_h.to(dev)
     Z = Z_h.to(dev)
-    Q = torch.empty((n, m), dtype=torch.float64, device=dev)
-    R = torch.empty((n, n), dtype=torch.float64, device=dev)
-    Q_h = pinned((n, m))
     R_h = pinned((n, n))
-    fn = oqr.VARIANTS[args.variant]
-    stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
@@ -235,7 +256,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        _, _, st = fn(A, Z, Q, R)
+        _, _, st = step(A, Z)
         assert st == 0, f"warm-up status {st}: {oqr.status_string(st)}"
 
     # ---- timed region: inputs resident in HBM ----
@@ -248,7 +269,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            statuses.append(fn(A, Z, Q, R)[2])
+            statuses.append(step(A, Z)[2])
         e1.record(stream)
         barrier()
     ms_total = e0.elapsed_time(e1)
@@ -259,7 +280,7 @@ def main():
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step = float(t_local.item()) / args.steps
-    value = world * fl / (ms_step * 1e-3) / 1e9
+    value = fl / (ms_step * 1e-3) / 1e9  # the whole problem, all ranks
 
     # ---- end to end through the public call with host buffers ----
     h2d = A_h.numel() * 8 + Z_h.numel() * 8
@@ -269,16 +290,16 @@ def main():
     for _ in range(args.e2e_steps):
         A.copy_(A_h, non_blocking=True)
         Z.copy_(Z_h, non_blocking=True)
-        st = fn(A, Z, Q, R)[2]
-        Q_h.copy_(Q, non_blocking=True)
-        R_h.copy_(R, non_blocking=True)
+        Qs, Rs, st = step(A, Z)
+        Q_h.copy_(Qs, non_blocking=True)
+        R_h.copy_(Rs, non_blocking=True)
         assert st == 0
     e1.record(stream)
     barrier()
     t_e2e = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = world * fl / (float(t_e2e.item()) * 1e-3) / 1e9
+    e2e_value = fl / (float(t_e2e.item()) * 1e-3) / 1e9
 
     if rank == 0:
         k1_ms = gram_ms / max(gram_launches, 1)
@@ -293,20 +314,21 @@ def main():
             except Exception:
                 pass
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only
             cpu, _, _ = cpu_oracle_sample(p)
         peaks = measured_peaks()
         line = {
             "metric": METRIC,
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"configs[{args.config}] oqr_{args.variant}: m={m}, n={n}, "
                                    f"kappa_A={c['kappa_a']:g}, kappa_Z={c['kappa_z']:g}",
                        "m": m, "n": n, "variant": args.variant,
                        "flops_per_step": fl, "flop_normalisation": "2m^2n+2mn^2 (PAPER.md:959-961)",
                        "l2": "inputs (A = %.1f GB) larger than L2; no flush" % (8 * m * m / 1e9),
-                       "parallelism": "replicas" if world > 1 else "single GPU"},
+                       "parallelism": (f"row-sharded x{world}: one n x n all-gather per step (NCCL), "
+                                       "fixed rank-order sum") if (world > 1 or args.sharded) else "single GPU"},
             "roofline": {"bound": "tensor", "kernel": "gram_fused (K1)", "achieved": achieved,
                          "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,

@@ -55,6 +55,9 @@ def _load():
         lib.oqr_gen_problem.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_uint64, ctypes.c_int, P, ctypes.c_int64, P, ctypes.c_int64,
                                         P, P, P, P, P, P, P, P, P]
+        lib.oqr_gen_A_rows.restype = ctypes.c_int
+        lib.oqr_gen_A_rows.argtypes = [ctypes.c_int64, ctypes.c_double, ctypes.c_uint64, ctypes.c_int64,
+                                       ctypes.c_int64, P, ctypes.c_int64]
         lib.oqr_gen_normal.restype = ctypes.c_double
         lib.oqr_gen_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
         _lib = lib
@@ -125,6 +128,24 @@ def problem(m: int, n: int, kappa_a: float, kappa_z: float, seed: int, ucase: st
     if rc != 0:
         raise ValueError(f"oqr_gen_problem rejected arguments (m={m}, n={n}, ucase={ucase})")
     return Problem(m, n, kappa_a, kappa_z, seed, ucase, A, Z, Yv, Tv, d, s, Yu, Tu, Yw, Tw, cols)
+
+
+def A_rows(m: int, kappa_a: float, seed: int, r0: int, r1: int, lda: int | None = None,
+           out: np.ndarray | None = None) -> np.ndarray:
+    """Rows [r0, r1) of the A that ``problem(m, ..., kappa_a, ..., seed)`` generates (bitwise the
+    same entries) as a column-major (r1-r0) x m block: C-contiguous array of shape (m, lda)."""
+    lda = (r1 - r0) if lda is None else lda
+    a = out if out is not None else np.empty((m, lda), dtype=np.float64)
+    assert a.shape == (m, lda) and a.dtype == np.float64 and a.flags.c_contiguous
+    rc = _load().oqr_gen_A_rows(m, float(kappa_a), seed, r0, r1, _ptr(a), lda)
+    if rc != 0:
+        raise ValueError(f"oqr_gen_A_rows rejected arguments (m={m}, rows=[{r0},{r1}))")
+    return a
+
+
+def config_A_rows(k: int, r0: int, r1: int, **kw) -> np.ndarray:
+    c = CONFIGS[k]
+    return A_rows(c["m"], c["kappa_a"], SEED_BASE + k, r0, r1, **kw)
 
 
 def config(k: int, ucase: str = "reflect", **kw) -> Problem:

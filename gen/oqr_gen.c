@@ -125,6 +125,84 @@ static void select_cols(int64_t m, int64_t n, int ucase, int64_t* J) {
   }
 }
 
+/* Per-row coefficients of the closed form of A = V diag(d) V^T (V = I - Y T Y^T):
+ * K = Y^T diag(d) Y, M = T K T^T, and for each row i: p_i = T y_i, q_i = T^T y_i, r_i = M y_i
+ * (P[i*12 + 0..3 | 4..7 | 8..11]).  Caller frees. */
+static double* a_prep(int64_t m, const double* Yv, const double* Tv, const double* d) {
+  double K[NREFL * NREFL], TK[NREFL * NREFL], M[NREFL * NREFL];
+  for (int a = 0; a < NREFL; a++)
+    for (int b = 0; b < NREFL; b++) {
+      double s = 0.0;
+      for (int64_t i = 0; i < m; i++) s += Yv[a * m + i] * d[i] * Yv[b * m + i];
+      K[b * NREFL + a] = s;
+    }
+  for (int a = 0; a < NREFL; a++)
+    for (int b = 0; b < NREFL; b++) {
+      double s = 0.0;
+      for (int c = 0; c < NREFL; c++) s += Tv[c * NREFL + a] * K[b * NREFL + c];
+      TK[b * NREFL + a] = s;
+    }
+  for (int a = 0; a < NREFL; a++)
+    for (int b = 0; b < NREFL; b++) {
+      double s = 0.0;
+      for (int c = 0; c < NREFL; c++) s += TK[c * NREFL + a] * Tv[c * NREFL + b];
+      M[b * NREFL + a] = s;
+    }
+  double* P = (double*)malloc(sizeof(double) * m * 3 * NREFL);
+  for (int64_t i = 0; i < m; i++) {
+    double* pi = P + i * 3 * NREFL;
+    for (int a = 0; a < NREFL; a++) {
+      double sp = 0.0, sq = 0.0, sr = 0.0;
+      for (int b = 0; b < NREFL; b++) {
+        double yb = Yv[b * m + i];
+        sp += Tv[b * NREFL + a] * yb;
+        sq += Tv[a * NREFL + b] * yb;
+        sr += M[b * NREFL + a] * yb;
+      }
+      pi[a] = sp;
+      pi[NREFL + a] = sq;
+      pi[2 * NREFL + a] = sr;
+    }
+  }
+  return P;
+}
+
+/* A_ij for i <= j: d_i delta_ij - d_i (T y_i).y_j - d_j (T^T y_i).y_j + (M y_i).y_j.
+ * The stored matrix uses this value for both (i, j) and (j, i): bitwise symmetric. */
+static inline double a_entry(const double* P, const double* Yv, const double* d, int64_t m, int64_t i,
+                             int64_t j) {
+  const double* pi = P + i * 3 * NREFL;
+  double t1 = 0.0, t2 = 0.0, t3 = 0.0;
+  for (int a = 0; a < NREFL; a++) {
+    const double yja = Yv[a * m + j];
+    t1 += pi[a] * yja;
+    t2 += pi[NREFL + a] * yja;
+    t3 += pi[2 * NREFL + a] * yja;
+  }
+  return (i == j ? d[i] : 0.0) - d[i] * t1 - d[j] * t2 + t3;
+}
+
+/* Rows [r0, r1) of the same A as oqr_gen_problem (bitwise identical entries), stored as an
+ * (r1 - r0) x m column-major block with leading dimension lda >= r1 - r0 -- the row shard of
+ * one rank in the row-sharded multi-GPU path.  Returns 0 or -1. */
+int oqr_gen_A_rows(int64_t m, double kappa_a, uint64_t seed, int64_t r0, int64_t r1, double* A, int64_t lda) {
+  if (m < 1 || kappa_a < 1.0 || r0 < 0 || r1 > m || r1 <= r0 || lda < r1 - r0 || !A) return -1;
+  double* Yv = (double*)malloc(sizeof(double) * m * NREFL);
+  double* d = (double*)malloc(sizeof(double) * m);
+  double Tv[NREFL * NREFL];
+  oqr_gen_wy(m, seed, 1, Yv, Tv);
+  oqr_gen_logspace(m, kappa_a, d);
+  double* P = a_prep(m, Yv, Tv, d);
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < m; j++)
+    for (int64_t i = r0; i < r1; i++)
+      A[j * lda + (i - r0)] = (i <= j) ? a_entry(P, Yv, d, m, i, j) : a_entry(P, Yv, d, m, j, i);
+  free(P);
+  free(Yv);
+  free(d);
+  return 0;
+}
+
 /*
  * Fill A (m x m, lda) and/or Z (m x n, ldz); either may be NULL.
  * Outputs (each may be NULL): Yv (m x 4), Tv (4 x 4) of V; d (m); s (n);
@@ -149,58 +227,11 @@ int oqr_gen_problem(int64_t m, int64_t n, double kappa_a, double kappa_z, uint64
   oqr_gen_logspace(m, kappa_a, d);
 
   if (A) {
-    /* K = Y^T diag(d) Y ; M = T K T^T (symmetric 4x4). */
-    double K[NREFL * NREFL], TK[NREFL * NREFL], M[NREFL * NREFL];
-    for (int a = 0; a < NREFL; a++)
-      for (int b = 0; b < NREFL; b++) {
-        double s = 0.0;
-        for (int64_t i = 0; i < m; i++) s += Yv[a * m + i] * d[i] * Yv[b * m + i];
-        K[b * NREFL + a] = s;
-      }
-    for (int a = 0; a < NREFL; a++)
-      for (int b = 0; b < NREFL; b++) {
-        double s = 0.0;
-        for (int c = 0; c < NREFL; c++) s += Tv[c * NREFL + a] * K[b * NREFL + c];
-        TK[b * NREFL + a] = s;
-      }
-    for (int a = 0; a < NREFL; a++)
-      for (int b = 0; b < NREFL; b++) {
-        double s = 0.0;
-        for (int c = 0; c < NREFL; c++) s += TK[c * NREFL + a] * Tv[c * NREFL + b];
-        M[b * NREFL + a] = s;
-      }
-    /* per row: p_i = T y_i, q_i = T^T y_i, r_i = M y_i */
-    double* P = (double*)malloc(sizeof(double) * m * 3 * NREFL);
-    for (int64_t i = 0; i < m; i++) {
-      double* pi = P + i * 3 * NREFL;
-      for (int a = 0; a < NREFL; a++) {
-        double sp = 0.0, sq = 0.0, sr = 0.0;
-        for (int b = 0; b < NREFL; b++) {
-          double yb = Yv[b * m + i];
-          sp += Tv[b * NREFL + a] * yb;
-          sq += Tv[a * NREFL + b] * yb;
-          sr += M[b * NREFL + a] * yb;
-        }
-        pi[a] = sp;
-        pi[NREFL + a] = sq;
-        pi[2 * NREFL + a] = sr;
-      }
-    }
-    /* A_ij = d_i delta_ij - d_i (T y_i).y_j - d_j (T^T y_i).y_j + (M y_i).y_j, i <= j, mirrored. */
+    double* P = a_prep(m, Yv, Tv, d);
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t j = 0; j < m; j++) {
-      double yj[NREFL];
-      for (int a = 0; a < NREFL; a++) yj[a] = Yv[a * m + j];
-      double dj = d[j];
       for (int64_t i = 0; i <= j; i++) {
-        const double* pi = P + i * 3 * NREFL;
-        double t1 = 0.0, t2 = 0.0, t3 = 0.0;
-        for (int a = 0; a < NREFL; a++) {
-          t1 += pi[a] * yj[a];
-          t2 += pi[NREFL + a] * yj[a];
-          t3 += pi[2 * NREFL + a] * yj[a];
-        }
-        double v = (i == j ? d[i] : 0.0) - d[i] * t1 - dj * t2 + t3;
+        const double v = a_entry(P, Yv, d, m, i, j);
         A[j * lda + i] = v;
         A[i * lda + j] = v;
       }

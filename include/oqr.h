@@ -110,6 +110,24 @@ int oqr_potrf(int64_t n, const double* G, double* R, int* d_info, oqr_stream_t s
 int oqr_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, double* Q,
              oqr_stream_t stream);
 
+/* ---- Row-sharded multi-GPU path.  Rank r holds rows
+ *      R_r = [r0, r0 + mr) of A and all of Z.  Because G = sum_r Z_{R_r}^T (A_{R_r,:} Z) for any
+ *      partition of the rows (bilinearity of Algorithm 1 lines 1-2), each rank
+ *      computes its partial with oqr_gram_rows, the partials are exchanged once (all-gather,
+ *      n x n each), every rank sums them in rank order with oqr_sum_partials (bitwise-identical G
+ *      and R everywhere), factors with oqr_potrf and solves its own rows with oqr_trsm. ---- */
+
+/* G_r = Z_{R}^T (A_{R,:} Z), R = rows [r0, r0 + mr) of A.  Ar: the row block, mr x m column-major,
+ * leading dimension ldar >= mr (element (i, j) of the block = A[r0 + i, j]); Z: all m rows, ldz >= m.
+ * G: n x n, ld n.  Asynchronous.  Status: 0, -1 m, -2 n, -3 Ar, -4 ldar, -5 Z, -6 ldz, -7 G,
+ * -9 row range, -100 CUDA, -101 workspace.  With r0 = 0, mr = m this equals oqr_gram. */
+int oqr_gram_rows(int64_t m, int64_t n, int64_t r0, int64_t mr, const double* Ar, int64_t ldar,
+                  const double* Z, int64_t ldz, double* G, oqr_stream_t stream);
+
+/* G = sum_{c=0}^{count-1} P_c in c order (fixed order => reproducible bits); P holds count
+ * consecutive n x n matrices (ld n), G is n x n (ld n).  Asynchronous. */
+int oqr_sum_partials(int64_t n, int64_t count, const double* P, double* G, oqr_stream_t stream);
+
 /* ---- Measurement hook: per-launch CUDA-event timing of the fused Gram kernel (K1).
  *      When enabled, every K1 launch is bracketed by events recorded on the caller's stream;
  *      oqr_timing_read returns the accumulated milliseconds and launch count since the last

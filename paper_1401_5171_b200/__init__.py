@@ -25,8 +25,8 @@ __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm"
 
 # Every symbol include/oqr.h declares.
 EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_status_string", "oqr_gram",
-           "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_timing_enable", "oqr_timing_reset",
-           "oqr_timing_read", "oqr_launch_count")
+           "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_gram_rows", "oqr_sum_partials",
+           "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_launch_count")
 
 
 class OqrError(RuntimeError):
@@ -61,6 +61,10 @@ def lib() -> ctypes.CDLL:
         L.oqr_potrf.argtypes = [I64, P, P, P, P]
         L.oqr_trsm.restype = I
         L.oqr_trsm.argtypes = [I64, I64, P, I64, P, P, P]
+        L.oqr_gram_rows.restype = I
+        L.oqr_gram_rows.argtypes = [I64, I64, I64, I64, P, I64, P, I64, P, P]
+        L.oqr_sum_partials.restype = I
+        L.oqr_sum_partials.argtypes = [I64, I64, P, P, P]
         L.oqr_timing_enable.restype = None
         L.oqr_timing_enable.argtypes = [I]
         L.oqr_timing_reset.restype = None
@@ -185,6 +189,48 @@ def trsm(Z, R, m: int | None = None, Q=None, stream=None):
         Q = torch.empty((n, m), dtype=torch.float64, device=Z.device)
     st = lib().oqr_trsm(m, n, _check(Z, "Z", m), Z.shape[1], _check(R, "R", n), _check(Q, "Q", m),
                         _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_trsm")
+    return Q
+
+
+def gram_rows(Ar, Z, r0: int, mr: int, G=None, stream=None):
+    """Partial Gram of a row shard: Z_R^T (A_{R,:} Z), R = [r0, r0 + mr).  Ar: (m, ldar) tensor
+    holding the mr x m row block column-major (ldar >= mr); Z: (n, ldz) with all m rows."""
+    import torch
+    n, m = Z.shape[0], Ar.shape[0]
+    if G is None:
+        G = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    st = lib().oqr_gram_rows(m, n, r0, mr, _check(Ar, "Ar", mr), Ar.shape[1], _check(Z, "Z", m), Z.shape[1],
+                             _check(G, "G", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_gram_rows")
+    return G
+
+
+def sum_partials(P, G=None, stream=None):
+    """G = sum_c P[c] in c order; P: (count, n, n) tensor of column-major n x n partials."""
+    import torch
+    count, n = P.shape[0], P.shape[1]
+    if not P.is_contiguous() or P.dtype != torch.float64 or not P.is_cuda:
+        raise TypeError("P: expected a contiguous float64 CUDA tensor (count, n, n)")
+    if G is None:
+        G = torch.empty((n, n), dtype=torch.float64, device=P.device)
+    st = lib().oqr_sum_partials(n, count, ctypes.c_void_p(P.data_ptr()), _check(G, "G", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_sum_partials")
+    return G
+
+
+def trsm_rows(Z, R, r0: int, mr: int, Q=None, stream=None):
+    """Q_local = Z[r0:r0+mr, :] R^{-1} (rows of a shard); Z: (n, ldz) with all rows; Q: (n, mr)."""
+    import torch
+    n = Z.shape[0]
+    if Q is None:
+        Q = torch.empty((n, mr), dtype=torch.float64, device=Z.device)
+    _check(Z, "Z", r0 + mr)
+    zp = ctypes.c_void_p(Z.data_ptr() + 8 * r0)
+    st = lib().oqr_trsm(mr, n, zp, Z.shape[1], _check(R, "R", n), _check(Q, "Q", mr), _stream(stream))
     if st:
         raise OqrError(st, "oqr_trsm")
     return Q

@@ -57,27 +57,30 @@ static void pool_keep_memory() {
 struct Workspace {
   double* base = nullptr;
   double* Zp = nullptr;    // packed Z (or Q1 / Y)
+  double* Zc = nullptr;    // packed local rows of Z (row-sharded Gram only)
   double* P = nullptr;     // per-CTA partial Gram slots
   double* G = nullptr;     // n x n Gram
   double* R1 = nullptr;    // n x n (R1 of normal2 / S of prequr)
   double* R2 = nullptr;    // n x n (R2 of normal2 / U of prequr)
   int* info = nullptr;
   cudaStream_t s = nullptr;
-  int alloc(int64_t m, int n, cudaStream_t st) {
+  int alloc(int64_t m, int n, cudaStream_t st, int64_t mr_local = 0) {
     pool_keep_memory();
     s = st;
     const int NP = 8 * (int)cdiv(n, 8);
     const size_t zp = (size_t)zp_doubles(m, NP);
+    const size_t zc = mr_local > 0 ? (size_t)zp_doubles(mr_local, NP) : 0;
     const size_t sl = slots_doubles(n, gram_grid(m));
     const size_t nn = (size_t)n * n;
-    const size_t total = zp + sl + 3 * nn + 2;  // +2 doubles (16 B) for info
+    const size_t total = zp + zc + sl + 3 * nn + 2;  // +2 doubles (16 B) for info
     if (cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), st) != cudaSuccess) {
       cudaGetLastError();
       base = nullptr;
       return -101;
     }
     Zp = base;
-    P = Zp + zp;
+    Zc = Zp + zp;
+    P = Zc + zc;
     G = P + sl;
     R1 = G + nn;
     R2 = R1 + nn;
@@ -125,7 +128,7 @@ static int gram_into(int64_t m, int n, const double* A, int64_t lda, const doubl
                      double* G, Workspace& ws, cudaStream_t s) {
   int g = 0;
   OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
-  OQR_TRY(launch_gram_fused(m, n, A, lda, ws.Zp, ws.P, &g, s));
+  OQR_TRY(launch_gram_fused(m, m, n, A, lda, ws.Zp, ws.Zp, ws.P, &g, s));
   OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s));
   return 0;
 }
@@ -227,6 +230,7 @@ const char* oqr_status_string(int status) {
     case -6: return "invalid argument 6 (ldz < m)";
     case -7: return "invalid argument 7 (Q null or not 8-byte aligned)";
     case -8: return "invalid argument 8 (R null or not 8-byte aligned)";
+    case -9: return "invalid row range (r0 < 0, mr < 1 or r0 + mr > m)";
     case -100: return "CUDA error";
     case -101: return "workspace allocation failed";
     default: return "unknown status";
@@ -242,6 +246,36 @@ int oqr_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z
   Workspace ws;
   if ((st = ws.alloc(m, (int)n, s))) return st;
   return gram_into(m, (int)n, A, lda, Z, ldz, G, ws, s);
+}
+
+int oqr_gram_rows(int64_t m, int64_t n, int64_t r0, int64_t mr, const double* Ar, int64_t ldar, const double* Z,
+                  int64_t ldz, double* G, oqr_stream_t stream) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m || n > OQR_NMAX) return -2;
+  if (r0 < 0 || mr < 1 || r0 + mr > m) return -9;
+  if (Ar == nullptr || !aligned(Ar, 8)) return -3;
+  if (ldar < mr) return -4;
+  if (Z == nullptr || !aligned(Z, 8)) return -5;
+  if (ldz < m) return -6;
+  if (G == nullptr) return -7;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int ni = (int)n;
+  Workspace ws;
+  int st = ws.alloc(m, ni, s, mr);
+  if (st) return st;
+  int g = 0;
+  OQR_TRY(launch_pack_z(m, ni, Z, ldz, ws.Zp, s));
+  OQR_TRY(launch_pack_z(mr, ni, Z + r0, ldz, ws.Zc, s));
+  OQR_TRY(launch_gram_fused(m, mr, ni, Ar, ldar, ws.Zp, ws.Zc, ws.P, &g, s));
+  OQR_TRY(launch_gram_reduce(ni, g, ws.P, G, ni, s));
+  return 0;
+}
+
+int oqr_sum_partials(int64_t n, int64_t count, const double* P, double* G, oqr_stream_t stream) {
+  if (n < 1 || n > OQR_NMAX) return -2;
+  if (count < 1 || count > (1 << 20)) return -3;
+  if (P == nullptr || G == nullptr) return -4;
+  return cuda_status(launch_sum_partials((int)n, (int)count, P, G, n, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 int oqr_gram_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* G, oqr_stream_t stream) {

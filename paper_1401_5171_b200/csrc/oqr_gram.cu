@@ -211,7 +211,7 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
 // tiles need nothing special: TMA zero-fills rows/columns >= m.  Otherwise the A tile is loaded
 // with plain loads and zero fill (correct, slow).
 template <int NT>
-__device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, const CUtensorMap* tmap,
+__device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr, const CUtensorMap* tmap,
                                             const double* __restrict__ A, int64_t lda,
                                             const double* __restrict__ Zp, double* As, uint64_t* bar,
                                             int lane, uint64_t pol_a, uint64_t pol_z, bool tma_ok) {
@@ -235,7 +235,7 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, const CUte
     for (int e = lane; e < BK * BM; e += 32) {
       const int k = e / BM, r = e - k * BM;
       double v = 0.0;
-      if (row0 + r < m && col0 + k < m) v = A[(col0 + k) * lda + row0 + r];
+      if (row0 + r < mr && col0 + k < m) v = A[(col0 + k) * lda + row0 + r];
       As[e] = v;
     }
     fence_proxy_async_smem();  // generic writes before later async-proxy writes to the slot
@@ -253,8 +253,10 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, const CUte
 // DMMA is predicated.  Unit bookkeeping is incremental int32 (no division in the loop):
 // (I, kb) is the unit being consumed, (Ii, kbi) the unit `stages` ahead that a refill loads.
 template <int NT, int NTL>
-__device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m, const double* __restrict__ A,
-                                              int64_t lda, const double* __restrict__ Zp, double* slot,
+__device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m, int64_t mr,
+                                              const double* __restrict__ A, int64_t lda,
+                                              const double* __restrict__ Zp, const double* __restrict__ Zc,
+                                              double* slot,
                                               double* red, double* ring, uint64_t* full, uint64_t* empty,
                                               unsigned* relcnt, int KB, int u0, int u1, int stages,
                                               bool tma_ok, int rg, int ch, int lane, uint64_t pol_a,
@@ -311,7 +313,7 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last && ui < u1) {
       mbar_wait(&empty[s], ph);
-      issue_stage<NT>(Ii, kbi, m, tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, tma_ok);
+      issue_stage<NT>(Ii, kbi, m, mr, tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, tma_ok);
     }
     ++ui;
     if (++kbi == KB) {
@@ -324,7 +326,7 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     }
     const bool panel_end = (++kb == KB);
     if (panel_end || u + 1 == u1) {
-      contract_panel<NT>(acc, (int64_t)I * BM, Zp, red, slot, first, rg, ch, lane, threadIdx.x);
+      contract_panel<NT>(acc, (int64_t)I * BM, Zc, red, slot, first, rg, ch, lane, threadIdx.x);
       first = false;
 #pragma unroll
       for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
@@ -343,9 +345,9 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
 // `stages` ahead, so `stages - 1` stages of compute cover the copy latency.
 template <int NT>
 __global__ void __launch_bounds__(NCW * 32, 1)
-gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, const double* __restrict__ A,
-                  int64_t lda, const double* __restrict__ Zp, double* __restrict__ P, int KB,
-                  int U, int stages, bool tma_ok) {
+gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t mr, const double* __restrict__ A,
+                  int64_t lda, const double* __restrict__ Zp, const double* __restrict__ Zc,
+                  double* __restrict__ P, int KB, int U, int stages, bool tma_ok) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
   constexpr int STAGE = BM * BK + NT * 4 * FRAG;  // doubles per pipeline stage
@@ -377,17 +379,17 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, const dou
   if (warp == 0) {
     for (int s = 0; s < stages && u0 + s < u1; ++s) {
       const int u = u0 + s, I = u / KB;
-      issue_stage<NT>(I, u - I * KB, m, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
+      issue_stage<NT>(I, u - I * KB, m, mr, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
                       tma_ok);
     }
   }
   double* slot = P + c * (int64_t)NP * NP;
   if (ch == 0)
-    consume_units<NT, NTW>(&tmap, m, A, lda, Zp, slot, red, ring, full, empty, relcnt, KB, u0, u1, stages,
-                           tma_ok, rg, ch, lane, pol_a, pol_z);
+    consume_units<NT, NTW>(&tmap, m, mr, A, lda, Zp, Zc, slot, red, ring, full, empty, relcnt, KB, u0, u1,
+                           stages, tma_ok, rg, ch, lane, pol_a, pol_z);
   else
-    consume_units<NT, NT - NTW>(&tmap, m, A, lda, Zp, slot, red, ring, full, empty, relcnt, KB, u0, u1,
-                                stages, tma_ok, rg, ch, lane, pol_a, pol_z);
+    consume_units<NT, NT - NTW>(&tmap, m, mr, A, lda, Zp, Zc, slot, red, ring, full, empty, relcnt, KB, u0,
+                                u1, stages, tma_ok, rg, ch, lane, pol_a, pol_z);
 }
 
 // ------------------------------------------------------------------ K4 --------------------
@@ -445,6 +447,13 @@ cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t
   return cudaGetLastError();
 }
 
+cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s) {
+  const int64_t total = (int64_t)n * n;
+  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, n, count, P, G, ldg);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ dispatch --------------
 static int num_sms() {
   int dev = 0, sms = 0;
@@ -486,13 +495,14 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// A as a 2-D FP64 tensor {rows m (contiguous), cols m (stride lda)}, box {BM, BK}, no swizzle,
+// A (or a row block of it) as a 2-D FP64 tensor {rows mr (contiguous), cols m (stride lda)},
+// box {BM, BK}, no swizzle,
 // out-of-bounds elements zero-filled.
-static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t m, int64_t lda) {
+static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t mr, int64_t m, int64_t lda) {
   if ((reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0 || m > (int64_t)INT32_MAX) return false;
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)m};
+  const cuuint64_t dims[2] = {(cuuint64_t)mr, (cuuint64_t)m};
   const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
   const cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)BK};
   const cuuint32_t estr[2] = {1, 1};
@@ -502,8 +512,8 @@ static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t m, int64_t ld
 }
 
 template <int NT>
-static cudaError_t gram_fused_nt(int64_t m, const double* A, int64_t lda, const double* Zp, double* P,
-                                 int* g_out, cudaStream_t s) {
+static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t lda, const double* Zp,
+                                 const double* Zc, double* P, int* g_out, cudaStream_t s) {
   size_t bytes;
   const int stages = fused_stages(NT, &bytes);
   static bool attr_done = false;  // per instantiation
@@ -513,17 +523,17 @@ static cudaError_t gram_fused_nt(int64_t m, const double* A, int64_t lda, const 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int64_t KB = cdiv(m, BK), U = cdiv(m, BM) * KB;  // U < 2^31 for every m that fits in HBM
+  const int64_t KB = cdiv(m, BK), U = cdiv(mr, BM) * KB;  // U < 2^31 for every m that fits in HBM
   if (U > (int64_t)INT32_MAX - 64) return cudaErrorInvalidValue;
   int64_t g = num_sms();
   if (g > U) g = U;
   *g_out = (int)g;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  const bool tma_ok = make_tmap_a(&tmap, A, m, lda);
+  const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda);
   timing_begin(s);
-  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, A, lda, Zp, P, (int)KB, (int)U, stages,
-                                                             tma_ok);
+  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, P, (int)KB, (int)U,
+                                                             stages, tma_ok);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);
@@ -545,11 +555,11 @@ static cudaError_t gram_euclid_nt(int64_t m, const double* Zp, double* P, int* g
   X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
 
-cudaError_t launch_gram_fused(int64_t m, int n, const double* A, int64_t lda, const double* Zp,
-                              double* P, int* g_out, cudaStream_t s) {
+cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int64_t lda, const double* Zp,
+                              const double* Zc, double* P, int* g_out, cudaStream_t s) {
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT) \
-  case NT: return gram_fused_nt<NT>(m, A, lda, Zp, P, g_out, s);
+  case NT: return gram_fused_nt<NT>(m, mr, A, lda, Zp, Zc, P, g_out, s);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

@@ -45,8 +45,13 @@ cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double
 // Per-CTA partial Gram slots P[g][NP][NP] of Z^T (A Z); returns the grid size used in *g_out.
 // A is moved by 2-D tensor TMA when it is 16-byte aligned with an even lda; otherwise by plain
 // loads (same results, slow).
-cudaError_t launch_gram_fused(int64_t m, int n, const double* A, int64_t lda, const double* Zp,
-                              double* P, int* g_out, cudaStream_t s);
+// Rows [0, mr) of A (or of a row block of A holding mr rows, all m columns): slots of
+// Z_rows^T (A_rows Z) where Zp packs all m rows of Z (B operand) and Zc packs the mr rows of Z
+// that match the A rows (contraction operand; Zc == Zp on one GPU).
+cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int64_t lda, const double* Zp,
+                              const double* Zc, double* P, int* g_out, cudaStream_t s);
+// G (n x n, ldg) = sum_{c<count} P_c, P_c = n x n (ld n) consecutive, c ascending.
+cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s);
 // Per-CTA partial slots of Z^T Z.
 cudaError_t launch_gram_euclid(int64_t m, int n, const double* Zp, double* P, int* g_out,
                                cudaStream_t s);

@@ -75,3 +75,12 @@ def test_configs_recipe():
     assert (p.m, p.n, p.kappa_a, p.kappa_z, p.seed) == (200, 10, 1e2, 1e2, 0x14015171)
     w = gen.witness(with_A=False)
     assert w.m == 10000 and w.n == 100 and w.ucase == "split"
+
+
+def test_A_rows_bitwise_equal_to_full_rows():
+    # the row shard of one rank (multi-GPU path) holds exactly the same bits as the full A
+    p = gen.problem(333, 7, 1e4, 1e2, 19)
+    full = _dense(p.A, 333)
+    for r0, r1 in ((0, 64), (64, 200), (200, 333), (17, 18)):
+        blk = gen.A_rows(333, 1e4, 19, r0, r1, lda=r1 - r0 + 2)
+        assert np.array_equal(blk[:, : r1 - r0].T, full[r0:r1, :])

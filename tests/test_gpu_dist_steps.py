@@ -1,0 +1,67 @@
+"""GPU kernels of the row-sharded path (oqr_gram_rows, oqr_sum_partials, oqr_trsm on row shards) on
+ONE device, shards processed one after another (no kernel waits for another), against the oracle:
+  * sum of the shard Grams = oqr_gram within 2 gamma_{3m} |Z|^T|A||Z| (T1; bilinearity of
+    Algorithm 1 lines 1-2); a single shard covering all rows is bitwise oqr_gram;
+  * the assembled Q, R meet the CHOLQR gates T2, T5 against the oracle."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from oracle import U, gamma
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def oqr():
+    import paper_1401_5171_b200 as m
+    m.lib()
+    return m
+
+
+@pytest.mark.parametrize("m,n,world", [(1000, 40, 2), (4000, 50, 3), (333, 21, 2), (2048, 200, 4)])
+def test_row_sharded_cholqr(oqr, m, n, world):
+    from paper_1401_5171_b200.dist import row_partition
+    ka, kz, seed = 1e3, 1e2, 41
+    p = gen.problem(m, n, ka, kz, seed)
+    Z = torch.from_numpy(p.Z).cuda()
+    parts = row_partition(m, world)
+    Gs = []
+    for r0, mr in parts:
+        ldar = mr + (mr & 1)  # even leading dimension: tensor-TMA path
+        Ar = torch.from_numpy(gen.A_rows(m, ka, seed, r0, r0 + mr, lda=ldar)).cuda()
+        Gs.append(oqr.gram_rows(Ar, Z, r0, mr))
+    G = oqr.sum_partials(torch.stack(Gs)).cpu().numpy().T
+    Go = oracle.from_cm(oracle.gram(p.A, p.Z, m), n)
+    Zd = np.abs(oracle.from_cm(p.Z, m))
+    M = Zd.T @ (np.abs(oracle.from_cm(p.A, m)) @ Zd)
+    assert np.all(np.abs(G - Go) <= 2 * gamma(3 * m) * M)
+    R, info = oqr.potrf(torch.from_numpy(oracle.to_cm(G)).cuda())
+    assert int(info.item()) == 0
+    Q = torch.cat([oqr.trsm_rows(Z, R, r0, mr) for r0, mr in parts], dim=1)
+    Qg, Rg = Q.cpu().numpy(), R.cpu().numpy()
+    assert oracle.componentwise_ratio(p.Z, Qg, Rg, m) <= gamma(n + 1)
+    Qo, Ro, sto = oracle.normal(p.A, p.Z, m)
+    E, Eo = oracle.orth_error(p.A, Qg, m), oracle.orth_error(p.A, Qo, m)
+    normQ = np.linalg.norm(oracle.from_cm(Qo, m), 2)
+    assert E <= 10 * Eo + 10 * n * U * float(np.max(p.d)) * normQ ** 2
+
+
+def test_single_shard_is_bitwise_oqr_gram(oqr):
+    p = gen.problem(1000, 30, 1e2, 1e2, 3)
+    A = torch.from_numpy(p.A).cuda()
+    Z = torch.from_numpy(p.Z).cuda()
+    assert torch.equal(oqr.gram_rows(A, Z, 0, 1000), oqr.gram(A, Z))
+
+
+def test_normal_rows_world1_matches_normal(oqr):
+    from paper_1401_5171_b200.dist import normal_rows
+    p = gen.problem(700, 33, 1e2, 1e2, 4)
+    A = torch.from_numpy(p.A).cuda()
+    Z = torch.from_numpy(p.Z).cuda()
+    Q1, R1, s1 = normal_rows(A, Z, 0, 700)
+    Q2, R2, s2 = oqr.normal(A, Z)
+    assert s1 == s2 == 0
+    assert torch.equal(R1, R2) and torch.equal(Q1, Q2)
