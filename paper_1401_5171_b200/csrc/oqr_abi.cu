@@ -137,7 +137,7 @@ static int gram_euclid_into(int64_t m, int n, const double* Z, int64_t ldz, doub
                             cudaStream_t s) {
   int g = 0;
   OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
-  OQR_TRY(launch_gram_euclid(m, n, ws.Zp, ws.P, &g, s));
+  OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zp, ws.P, &g, s));
   OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s));
   return 0;
 }

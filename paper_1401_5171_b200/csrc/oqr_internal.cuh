@@ -52,8 +52,8 @@ cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int
                               const double* Zc, double* P, int* g_out, cudaStream_t s);
 // G (n x n, ldg) = sum_{c<count} P_c, P_c = n x n (ld n) consecutive, c ascending.
 cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s);
-// Per-CTA partial slots of Z^T Z.
-cudaError_t launch_gram_euclid(int64_t m, int n, const double* Zp, double* P, int* g_out,
+// Slots of X^T Y for two packed m x n operands (X = Y = Zp: the Euclidean Gram).
+cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
                                cudaStream_t s);
 // G (n x n, ldg) = sum_{c<g} P[c] in fixed c order.
 cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s);

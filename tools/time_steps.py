@@ -34,6 +34,7 @@ R, info = oqr.potrf(G)
 torch.cuda.synchronize()
 assert int(info.item()) == 0
 res = {"gram (pack+K1+K1r)": timed(lambda: oqr.gram(A, Z, G)),
+       "gram_euclid (pack+K4+K1r)": timed(lambda: oqr.gram_euclid(Z, m=m)),
        "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)),
        "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
 for v in ("normal", "normal2", "prequr"):
