@@ -148,6 +148,46 @@ def config_A_rows(k: int, r0: int, r1: int, **kw) -> np.ndarray:
     return A_rows(c["m"], c["kappa_a"], SEED_BASE + k, r0, r1, **kw)
 
 
+# NEXT-N3 tridiagonal workload (A tridiagonal, m = 100000, n varied).
+# The paper does not give the entries of its tridiagonal A; we use the shifted 1-D Laplacian
+# T = tridiag(-1, 2 + c, -1) with c chosen so that kappa(T) is exactly kappa_A (R18).
+TRIDIAG_CONFIGS = {
+    "T": dict(m=100000, n=200, kappa_a=1e3, kappa_z=1e2),      # bench / full-size parity
+    "t": dict(m=2000, n=30, kappa_a=1e3, kappa_z=1e2),         # small parity case
+}
+
+
+def tridiag(m: int, kappa_a: float):
+    """(d, e): diagonal (m) and off-diagonal (m-1) of T = tridiag(-1, 2 + c, -1), whose eigenvalues
+    are lambda_k = c + 2 - 2 cos(k pi / (m + 1)) with eigenvectors sqrt(2/(m+1)) sin(i k pi/(m+1));
+    c = 2 cos(pi/(m+1)) (kappa+1)/(kappa-1) - 2 makes lambda_m / lambda_1 = kappa_A.
+    Input generation only (closed form, no method arithmetic)."""
+    C = np.cos(np.pi / (m + 1))
+    c = 2.0 * C * (kappa_a + 1.0) / (kappa_a - 1.0) - 2.0 if kappa_a > 1.0 else 0.0
+    d = np.full(m, 2.0 + c)
+    e = np.full(max(m - 1, 0), -1.0)
+    return d, e
+
+
+def tridiag_eigen(m: int, kappa_a: float, ks):
+    """Exact eigenvalues lambda_k and unit eigenvectors (m x len(ks)) of tridiag(m, kappa_a), k 1-based."""
+    C = np.cos(np.pi / (m + 1))
+    c = 2.0 * C * (kappa_a + 1.0) / (kappa_a - 1.0) - 2.0 if kappa_a > 1.0 else 0.0
+    ks = np.asarray(ks, dtype=np.float64)
+    lam = c + 2.0 - 2.0 * np.cos(ks * np.pi / (m + 1))
+    i = np.arange(1, m + 1, dtype=np.float64)[:, None]
+    V = np.sqrt(2.0 / (m + 1)) * np.sin(i * ks[None, :] * np.pi / (m + 1))
+    return lam, V
+
+
+def tridiag_config(key: str, **kw):
+    """(d, e, Problem with Z only) for TRIDIAG_CONFIGS[key]; Z as in the dense configs (ucase reflect)."""
+    c = TRIDIAG_CONFIGS[key]
+    d, e = tridiag(c["m"], c["kappa_a"])
+    p = problem(c["m"], c["n"], c["kappa_a"], c["kappa_z"], SEED_BASE + 0x7D, with_A=False, **kw)
+    return d, e, p
+
+
 def config(k: int, ucase: str = "reflect", **kw) -> Problem:
     c = CONFIGS[k]
     return problem(c["m"], c["n"], c["kappa_a"], c["kappa_z"], SEED_BASE + k, ucase=ucase, **kw)

@@ -61,6 +61,11 @@ def _load():
             "orc_dd_resid": (None, [I, I, P, I, P, I, P, I, P, P]),
             "orc_dd_chol_resid": (None, [I, P, I, P, I, P, P]),
             "orc_dd_orth_cols": (None, [I, I, P, P, I, P, I, P]),
+            "orc_gram_tridiag": (None, [I, I, P, P, P, I, P, I]),
+            "orc_normal_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
+            "orc_normal2_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
+            "orc_prequr_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
+            "orc_dd_orth_tridiag": (None, [I, I, P, P, P, I, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -252,3 +257,63 @@ def chol_backward_ratio(G_dense: np.ndarray, R_store: np.ndarray) -> float:
     num = np.abs(D[iu])
     mask = den > 0
     return float((num[mask] / den[mask]).max()) if mask.any() else 0.0
+
+
+# ------------------------------------------------ tridiagonal A (NEXT-N3) ---
+def _vec(v):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    return v if v.size else np.zeros(1)
+
+
+def gram_tridiag(d, e, Z, m):
+    """G = Z^T (T Z), T = tridiag(e, d, e); storage (n, n)."""
+    Z, ldz = _cm(Z, m)
+    n = Z.shape[0]
+    G = np.empty((n, n))
+    d, e = _vec(d), _vec(e)
+    _load().orc_gram_tridiag(m, n, _p(d), _p(e), _p(Z), ldz, _p(G), n)
+    return G
+
+
+def _variant_tridiag(fn, d, e, Z, m):
+    Z, ldz = _cm(Z, m)
+    n = Z.shape[0]
+    Q = np.zeros((n, m))
+    R = np.zeros((n, n))
+    d, e = _vec(d), _vec(e)
+    info = getattr(_load(), fn)(m, n, _p(d), _p(e), _p(Z), ldz, _p(Q), _p(R))
+    return Q, R, info
+
+
+def normal_tridiag(d, e, Z, m):
+    return _variant_tridiag("orc_normal_tridiag", d, e, Z, m)
+
+
+def normal2_tridiag(d, e, Z, m):
+    return _variant_tridiag("orc_normal2_tridiag", d, e, Z, m)
+
+
+def prequr_tridiag(d, e, Z, m):
+    return _variant_tridiag("orc_prequr_tridiag", d, e, Z, m)
+
+
+VARIANTS_TRIDIAG = {"normal": normal_tridiag, "normal2": normal2_tridiag, "prequr": prequr_tridiag}
+
+
+def orth_error_tridiag(d, e, Q, m) -> float:
+    """||Q^T T Q - I||_2, check formed in double-double."""
+    Q, ldq = _cm(Q, m)
+    n = Q.shape[0]
+    E = np.empty((n, n))
+    d, e = _vec(d), _vec(e)
+    _load().orc_dd_orth_tridiag(m, n, _p(d), _p(e), _p(Q), ldq, _p(E))
+    return float(np.linalg.norm(E.T, 2))
+
+
+def densify_tridiag(d, e):
+    """Dense column-major storage (m, m) of tridiag(e, d, e) (for pins and small checks)."""
+    m = len(d)
+    A = np.diag(np.asarray(d, dtype=np.float64))
+    if m > 1:
+        A += np.diag(np.asarray(e, dtype=np.float64), 1) + np.diag(np.asarray(e, dtype=np.float64), -1)
+    return to_cm(A)

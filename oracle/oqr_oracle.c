@@ -364,3 +364,107 @@ void orc_dd_orth_cols(int64_t m, int64_t ns, const int64_t* cols, const double* 
     }
   free(AQ);
 }
+
+/* ========================================================================= */
+/* NEXT-N3: symmetric tridiagonal A = tridiag(e, d, e). */
+/* B = A Z by the 3-point definition, terms in ascending column order j = i-1, i, */
+/* i+1 starting from 0.0 -- the same operations as orc_gram on the densified A   */
+/* (whose other terms add exact zeros), so the two agree bitwise (pinned).       */
+/* ========================================================================= */
+void orc_gram_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                      double* G, int64_t ldg) {
+  double* B = (double*)malloc(sizeof(double) * m * n);
+#pragma omp parallel for schedule(static)
+  for (int64_t l = 0; l < n; l++) {
+    const double* z = Z + l * ldz;
+    for (int64_t i = 0; i < m; i++) {
+      double b = 0.0;
+      if (i > 0) b += e[i - 1] * z[i - 1];
+      b += d[i] * z[i];
+      if (i < m - 1) b += e[i] * z[i + 1];
+      B[l * m + i] = b;
+    }
+  }
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      const double* zk = Z + k * ldz;
+      const double* bl = B + l * m;
+      double s = 0.0;
+      for (int64_t i = 0; i < m; i++) s += zk[i] * bl[i];
+      G[l * ldg + k] = s;
+    }
+  free(B);
+}
+
+/* Algorithm 1 with the tridiagonal Gram. */
+int orc_normal_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                       double* Q, double* R) {
+  double* G = (double*)malloc(sizeof(double) * n * n);
+  orc_gram_tridiag(m, n, d, e, Z, ldz, G, n);
+  int info = orc_potrf(n, G, n, R, n);
+  free(G);
+  if (info) return info;
+  orc_trsm(m, n, Z, ldz, R, n, Q, m);
+  return 0;
+}
+
+/* Repeated CHOLQR (reading R1) with the tridiagonal Gram. */
+int orc_normal2_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                        double* Q, double* R) {
+  double* R1 = (double*)malloc(sizeof(double) * n * n);
+  double* R2 = (double*)malloc(sizeof(double) * n * n);
+  double* Q1 = (double*)malloc(sizeof(double) * m * n);
+  int info = orc_normal_tridiag(m, n, d, e, Z, ldz, Q1, R1);
+  if (!info) {
+    int info2 = orc_normal_tridiag(m, n, d, e, Q1, m, Q, R2);
+    if (info2) info = (int)n + info2;
+    else orc_trmm(n, R2, n, R1, n, R, n);
+  }
+  free(R1); free(R2); free(Q1);
+  return info;
+}
+
+/* PRE-CHOLQR (Algorithm 2, reading R2) with the tridiagonal A-stage. */
+int orc_prequr_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                       double* Q, double* R) {
+  double* G = (double*)malloc(sizeof(double) * n * n);
+  double* S = (double*)malloc(sizeof(double) * n * n);
+  double* U = (double*)malloc(sizeof(double) * n * n);
+  double* Y = (double*)malloc(sizeof(double) * m * n);
+  orc_gram_euclid(m, n, Z, ldz, G, n);
+  int info = orc_potrf(n, G, n, S, n);
+  if (!info) {
+    orc_trsm(m, n, Z, ldz, S, n, Y, m);
+    int info2 = orc_normal_tridiag(m, n, d, e, Y, m, Q, U);
+    if (info2) info = (int)n + info2;
+    else orc_trmm(n, U, n, S, n, R, n);
+  }
+  free(G); free(S); free(U); free(Y);
+  return info;
+}
+
+/* E = Q^T A Q - I for tridiagonal A, double-double (the same checker as orc_dd_orth). */
+void orc_dd_orth_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Q, int64_t ldq,
+                         double* E) {
+  dd_t* AQ = (dd_t*)malloc(sizeof(dd_t) * m * n);
+#pragma omp parallel for schedule(static)
+  for (int64_t l = 0; l < n; l++) {
+    const double* q = Q + l * ldq;
+    for (int64_t i = 0; i < m; i++) {
+      dd_t s = {0.0, 0.0};
+      if (i > 0) s = dd_add_prod(s, e[i - 1], q[i - 1]);
+      s = dd_add_prod(s, d[i], q[i]);
+      if (i < m - 1) s = dd_add_prod(s, e[i], q[i + 1]);
+      AQ[l * m + i] = s;
+    }
+  }
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      dd_t s = {k == l ? -1.0 : 0.0, 0.0};
+      for (int64_t i = 0; i < m; i++) s = dd_add_dd_prod(s, Q[k * ldq + i], AQ[l * m + i]);
+      E[l * n + k] = s.hi + s.lo;
+    }
+  free(AQ);
+}
