@@ -82,6 +82,21 @@ int oqr_normal2(int64_t m, int64_t n, const double* A, int64_t lda, const double
 int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                double* Q, double* R, oqr_stream_t stream);
 
+/*
+ * Tridiagonal A (the paper's second workload):
+ * A = tridiag(e, d, e) symmetric positive definite, d: m diagonal entries, e: m-1 off-diagonal
+ * entries (device pointers; e may be NULL when m == 1).  Same algorithms, outputs and status
+ * codes as the dense calls; argument codes: -1 m, -2 n, -3 d, -4 e, -5 Z, -6 ldz, -7 Q, -8 R.
+ * The A-product is the 3-point stencil (O(mn)), fused into the packing of the Gram operand;
+ * the Gram Z^T (A Z) then runs on the FP64 tensor pipe.  Synchronous, like oqr_normal.
+ */
+int oqr_normal_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                       double* Q, double* R, oqr_stream_t stream);
+int oqr_normal2_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z,
+                        int64_t ldz, double* Q, double* R, oqr_stream_t stream);
+int oqr_prequr_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                       double* Q, double* R, oqr_stream_t stream);
+
 /* Human-readable text for a status code (static storage; never NULL). */
 const char* oqr_status_string(int status);
 
@@ -94,6 +109,10 @@ const char* oqr_status_string(int status);
  * fixed for a given (m, n, SM count), so repeated calls are bitwise identical. */
 int oqr_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
              double* G, oqr_stream_t stream);
+
+/* G = Z^T (T Z) for tridiagonal T = tridiag(e, d, e) (asynchronous step export). */
+int oqr_gram_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                     double* G, oqr_stream_t stream);
 
 /* G = Z^T Z, the Euclidean Gram of the PRE-CHOLQR pre-step (reading R2). */
 int oqr_gram_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* G,

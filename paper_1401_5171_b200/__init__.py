@@ -24,7 +24,8 @@ __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm"
            "launch_count", "EXPORTS"]
 
 # Every symbol include/oqr.h declares.
-EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_status_string", "oqr_gram",
+EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_tridiag", "oqr_normal2_tridiag",
+           "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
            "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_gram_rows", "oqr_sum_partials",
            "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_launch_count")
 
@@ -51,6 +52,12 @@ def lib() -> ctypes.CDLL:
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, I64, P, I64, P, P, P]
+        for name in ("oqr_normal_tridiag", "oqr_normal2_tridiag", "oqr_prequr_tridiag"):
+            f = getattr(L, name)
+            f.restype = I
+            f.argtypes = [I64, I64, P, P, P, I64, P, P, P]
+        L.oqr_gram_tridiag.restype = I
+        L.oqr_gram_tridiag.argtypes = [I64, I64, P, P, P, I64, P, P]
         L.oqr_status_string.restype = ctypes.c_char_p
         L.oqr_status_string.argtypes = [I]
         L.oqr_gram.restype = I
@@ -137,6 +144,59 @@ def prequr(A, Z, Q=None, R=None, stream=None, check: bool = True):
 
 
 VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr}
+
+
+def _vec(t, name: str, length: int):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda or t.dim() != 1:
+        raise TypeError(f"{name}: expected a 1-D float64 CUDA tensor")
+    if t.numel() < length or not t.is_contiguous():
+        raise ValueError(f"{name}: expected {length} contiguous entries")
+    return ctypes.c_void_p(t.data_ptr()) if length > 0 else ctypes.c_void_p(None)
+
+
+def _variant_tridiag(fname: str, d, e, Z, Q=None, R=None, stream=None, check: bool = True):
+    import torch
+    m, n = d.numel(), Z.shape[0]
+    pd, pe = _vec(d, "d", m), _vec(e, "e", m - 1)
+    pZ = _check(Z, "Z", m)
+    if Q is None:
+        Q = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    st = getattr(lib(), fname)(m, n, pd, pe, pZ, Z.shape[1], _check(Q, "Q", m), _check(R, "R", n), _stream(stream))
+    if check and st < 0:
+        raise OqrError(st, fname)
+    return Q, R, st
+
+
+def normal_tridiag(d, e, Z, Q=None, R=None, stream=None, check: bool = True):
+    """CHOLQR with tridiagonal A = tridiag(e, d, e) (NEXT-N3)."""
+    return _variant_tridiag("oqr_normal_tridiag", d, e, Z, Q, R, stream, check)
+
+
+def normal2_tridiag(d, e, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant_tridiag("oqr_normal2_tridiag", d, e, Z, Q, R, stream, check)
+
+
+def prequr_tridiag(d, e, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant_tridiag("oqr_prequr_tridiag", d, e, Z, Q, R, stream, check)
+
+
+VARIANTS_TRIDIAG = {"normal": normal_tridiag, "normal2": normal2_tridiag, "prequr": prequr_tridiag}
+
+
+def gram_tridiag(d, e, Z, G=None, stream=None):
+    """G = Z^T (T Z) for T = tridiag(e, d, e) (asynchronous step export)."""
+    import torch
+    m, n = d.numel(), Z.shape[0]
+    if G is None:
+        G = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    st = lib().oqr_gram_tridiag(m, n, _vec(d, "d", m), _vec(e, "e", m - 1), _check(Z, "Z", m), Z.shape[1],
+                                _check(G, "G", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_gram_tridiag")
+    return G
 
 
 def gram(A, Z, G=None, stream=None):

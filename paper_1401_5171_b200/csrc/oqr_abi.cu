@@ -123,12 +123,27 @@ static int check_args(int64_t m, int64_t n, const double* A, int64_t lda, const 
   return 0;
 }
 
-// G (ld n) = Z^T A Z through the packed copy of Z held in ws.Zp.
-static int gram_into(int64_t m, int n, const double* A, int64_t lda, const double* Z, int64_t ldz,
-                     double* G, Workspace& ws, cudaStream_t s) {
+// The SPD operator A of the inner product: dense (A, lda) or symmetric tridiagonal (d, e).
+struct AOp {
+  const double* A = nullptr;
+  int64_t lda = 0;
+  const double* d = nullptr;
+  const double* e = nullptr;
+  bool tridiag = false;
+};
+
+// G (ld n) = Z^T A Z through the packed copy of Z held in ws.Zp (and, for tridiagonal A, the
+// packed W = T Z in ws.Zc).
+static int gram_into(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* G, Workspace& ws,
+                     cudaStream_t s) {
   int g = 0;
   OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
-  OQR_TRY(launch_gram_fused(m, m, n, A, lda, ws.Zp, ws.Zp, ws.P, &g, s));
+  if (op.tridiag) {
+    OQR_TRY(launch_pack_w_tridiag(m, n, op.d, op.e, Z, ldz, ws.Zc, s));
+    OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zc, ws.P, &g, s));
+  } else {
+    OQR_TRY(launch_gram_fused(m, m, n, op.A, op.lda, ws.Zp, ws.Zp, ws.P, &g, s));
+  }
   OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s));
   return 0;
 }
@@ -144,9 +159,9 @@ static int gram_euclid_into(int64_t m, int n, const double* Z, int64_t ldz, doub
 
 // One CHOLQR pass: G = Z^T A Z; Rout = chol(G) (info = info_off + k on breakdown);
 // Q = Z Rout^{-1} (Z may be Q itself when ldz == m).
-static int cholqr_pass(int64_t m, int n, const double* A, int64_t lda, const double* Z, int64_t ldz,
-                       double* Q, double* Rout, int info_off, Workspace& ws, cudaStream_t s) {
-  int st = gram_into(m, n, A, lda, Z, ldz, ws.G, ws, s);
+static int cholqr_pass(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* Rout,
+                       int info_off, Workspace& ws, cudaStream_t s) {
+  int st = gram_into(op, m, n, Z, ldz, ws.G, ws, s);
   if (st) return st;
   OQR_TRY(launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s));
   OQR_TRY(launch_trsm(m, n, Z, ldz, Rout, n, Q, m, ws.info, s));
@@ -164,58 +179,132 @@ static int finish(Workspace& ws, cudaStream_t s) {
 
 using namespace oqr;
 
+namespace oqr {
+
+static int run_normal(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
+                      cudaStream_t s) {
+  Workspace ws;
+  int st = ws.alloc(m, n, s, op.tridiag ? m : 0);
+  if (st) return st;
+  if ((st = cholqr_pass(op, m, n, Z, ldz, Q, R, 0, ws, s))) return st;
+  return finish(ws, s);
+}
+
+static int run_normal2(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
+                       cudaStream_t s) {
+  Workspace ws;
+  int st = ws.alloc(m, n, s, op.tridiag ? m : 0);
+  if (st) return st;
+  // pass 1: [Q1, R1] = CHOLQR(A, Z), Q1 into Q
+  if ((st = cholqr_pass(op, m, n, Z, ldz, Q, ws.R1, 0, ws, s))) return st;
+  // pass 2: [Q, R2] = CHOLQR(A, Q1) in place; breakdown code n + k
+  if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
+  // R = R2 R1
+  if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R1, R, ws.info, s)))) return st;
+  return finish(ws, s);
+}
+
+static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
+                      cudaStream_t s) {
+  Workspace ws;
+  int st = ws.alloc(m, n, s, op.tridiag ? m : 0);
+  if (st) return st;
+  // pre-step: S = chol(Z^T Z), Y = Z S^{-1} (into Q)
+  if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
+  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s)))) return st;
+  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s)))) return st;
+  // A-stage: [Q, U] = CHOLQR(A, Y) in place; breakdown code n + k
+  if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
+  // R = U S
+  if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R1, R, ws.info, s)))) return st;
+  return finish(ws, s);
+}
+
+static AOp dense_op(const double* A, int64_t lda) {
+  AOp op;
+  op.A = A;
+  op.lda = lda;
+  return op;
+}
+
+static int check_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                         const double* Q, const double* R, bool needQR) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m || n > OQR_NMAX) return -2;
+  if (d == nullptr || !aligned(d, 8)) return -3;
+  if (m > 1 && (e == nullptr || !aligned(e, 8))) return -4;
+  if (Z == nullptr || !aligned(Z, 8)) return -5;
+  if (ldz < m) return -6;
+  if (needQR) {
+    if (Q == nullptr || !aligned(Q, 8)) return -7;
+    if (R == nullptr || !aligned(R, 8)) return -8;
+  }
+  return 0;
+}
+
+static AOp tridiag_op(const double* d, const double* e) {
+  AOp op;
+  op.d = d;
+  op.e = e;
+  op.tridiag = true;
+  return op;
+}
+
+}  // namespace oqr
+
 extern "C" {
 
 int oqr_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int res;
-  {
-    Workspace ws;
-    if ((st = ws.alloc(m, (int)n, s))) return st;
-    st = cholqr_pass(m, (int)n, A, lda, Z, ldz, Q, R, 0, ws, s);
-    if (st) return st;
-    res = finish(ws, s);
-  }
-  return res;
+  return run_normal(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_normal2(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                 double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int ni = (int)n;
-  Workspace ws;
-  if ((st = ws.alloc(m, ni, s))) return st;
-  // pass 1: [Q1, R1] = CHOLQR(A, Z), Q1 into Q
-  if ((st = cholqr_pass(m, ni, A, lda, Z, ldz, Q, ws.R1, 0, ws, s))) return st;
-  // pass 2: [Q, R2] = CHOLQR(A, Q1) in place; breakdown code n + k
-  if ((st = cholqr_pass(m, ni, A, lda, Q, m, Q, ws.R2, ni, ws, s))) return st;
-  // R = R2 R1
-  if ((st = cuda_status(launch_trmm(ni, ws.R2, ws.R1, R, ws.info, s)))) return st;
-  return finish(ws, s);
+  return run_normal2(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
+  return run_prequr(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_normal_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                       double* Q, double* R, oqr_stream_t stream) {
+  int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
+  if (st) return st;
+  return run_normal(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_normal2_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                        double* Q, double* R, oqr_stream_t stream) {
+  int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
+  if (st) return st;
+  return run_normal2(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_prequr_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                       double* Q, double* R, oqr_stream_t stream) {
+  int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
+  if (st) return st;
+  return run_prequr(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_gram_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                     double* G, oqr_stream_t stream) {
+  int st = check_tridiag(m, n, d, e, Z, ldz, nullptr, nullptr, false);
+  if (st) return st;
+  if (G == nullptr) return -7;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int ni = (int)n;
   Workspace ws;
-  if ((st = ws.alloc(m, ni, s))) return st;
-  // pre-step: S = chol(Z^T Z), Y = Z S^{-1} (into Q)
-  if ((st = gram_euclid_into(m, ni, Z, ldz, ws.G, ws, s))) return st;
-  if ((st = cuda_status(launch_potrf(ni, ws.G, ni, ws.R1, ni, ws.info, 0, s)))) return st;
-  if ((st = cuda_status(launch_trsm(m, ni, Z, ldz, ws.R1, ni, Q, m, ws.info, s)))) return st;
-  // A-stage: [Q, U] = CHOLQR(A, Y) in place; breakdown code n + k
-  if ((st = cholqr_pass(m, ni, A, lda, Q, m, Q, ws.R2, ni, ws, s))) return st;
-  // R = U S
-  if ((st = cuda_status(launch_trmm(ni, ws.R2, ws.R1, R, ws.info, s)))) return st;
-  return finish(ws, s);
+  if ((st = ws.alloc(m, (int)n, s, m))) return st;
+  return gram_into(tridiag_op(d, e), m, (int)n, Z, ldz, G, ws, s);
 }
 
 const char* oqr_status_string(int status) {
@@ -245,7 +334,7 @@ int oqr_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   Workspace ws;
   if ((st = ws.alloc(m, (int)n, s))) return st;
-  return gram_into(m, (int)n, A, lda, Z, ldz, G, ws, s);
+  return gram_into(dense_op(A, lda), m, (int)n, Z, ldz, G, ws, s);
 }
 
 int oqr_gram_rows(int64_t m, int64_t n, int64_t r0, int64_t mr, const double* Ar, int64_t ldar, const double* Z,
