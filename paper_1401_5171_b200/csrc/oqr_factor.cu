@@ -138,23 +138,32 @@ __device__ __forceinline__ void dmma_f(double (&d)[2], double a, double b) {
 
 // R is staged once per (persistent) CTA in shared memory in DMMA B-fragment order:
 //   Rt[((jt*(jt-1)/2 + kt)*2 + h)*32 + lane] = R[kt*8 + 4h + lane%4, jt*8 + lane/4]   (kt < jt)
-//   Rd[(jt*8 + c)*8 + c2] = R[jt*8 + c, jt*8 + c2]  (diagonal tiles; 1 on the diagonal beyond n)
-// so every fragment load is 256 consecutive bytes.  NT = 30 does not fit (238 KB) and gathers
-// its fragments from global memory (L2) instead.
+//   Rd[(jt*8 + c)*8 + c2] = R[jt*8 + c, jt*8 + c2]  (diagonal tiles, upper part)
+//   Ri[jt*8 + c] = 1 / R[jt*8 + c, jt*8 + c]       (1 beyond n)
+// so every fragment load is 256 consecutive bytes.  At NT = 30 Rd does not fit as well (238 KB):
+// the diagonal tiles are then read from global memory (L1/L2).
+// Diagonal 8 x 8 block: the row's 8 partial values are gathered into all 4 lanes of the row's
+// quad (8 independent shuffles) and each lane solves the row redundantly with an FMA chain,
+// q_c = (t_c - sum_{c'<c} q_c' r_c'c) * (1 / r_cc): no shuffles and no divisions on the chain.
+// (Multiplying by the rounded reciprocal adds one rounding per entry: the row-wise backward error
+// becomes |dR^i| <= gamma_{n+1} |R|, the bound the parity gates use.)
 constexpr int TRSM_THREADS = 256;  // 8 warps: <= 255 registers, the q fragments stay in registers
 
 template <int NT>
-constexpr size_t trsm_smem_doubles() { return (size_t)NT * (NT - 1) / 2 * 64 + (size_t)NT * 64; }
+constexpr size_t trsm_smem_doubles(bool with_rd) {
+  return (size_t)NT * (NT - 1) / 2 * 64 + (size_t)NT * 8 + (with_rd ? (size_t)NT * 64 : 0);
+}
 
-template <int NT, bool SMEM_R>
+template <int NT, bool SMEM_RD>
 __global__ void __launch_bounds__(TRSM_THREADS, 1)
 trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q (in place)
                  const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info) {
   if (info != nullptr && *info != 0) return;
   extern __shared__ __align__(16) double rsm[];
   double* const Rt_base = rsm;
-  double* const Rd_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
-  if (SMEM_R) {
+  double* const Ri_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
+  double* const Rd_base = Ri_base + (size_t)NT * 8;
+  {
     double* Rt = Rt_base;
     double* Rd = Rd_base;
     for (int jt = 1; jt < NT; ++jt) {  // tiles (kt < jt) of column tile jt: jt*64 doubles
@@ -165,13 +174,17 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
         dst[e] = (col < n) ? R[(int64_t)col * ldr + k] : 0.0;
       }
     }
-    for (int e = threadIdx.x; e < NT * 64; e += blockDim.x) {
-      const int jt = e >> 6, c = (e >> 3) & 7, c2 = e & 7;
-      const int r = jt * 8 + c, col = jt * 8 + c2;
-      double v = 0.0;
-      if (c <= c2) v = (col < n) ? R[(int64_t)col * ldr + r] : (c == c2 ? 1.0 : 0.0);
-      Rd[e] = v;
+    if (SMEM_RD) {
+      for (int e = threadIdx.x; e < NT * 64; e += blockDim.x) {
+        const int jt = e >> 6, c = (e >> 3) & 7, c2 = e & 7;
+        const int r = jt * 8 + c, col = jt * 8 + c2;
+        double v = 0.0;
+        if (c <= c2) v = (col < n) ? R[(int64_t)col * ldr + r] : (c == c2 ? 1.0 : 0.0);
+        Rd[e] = v;
+      }
     }
+    for (int e = threadIdx.x; e < NT * 8; e += blockDim.x)
+      Ri_base[e] = (e < n) ? 1.0 / R[(int64_t)e * ldr + e] : 1.0;
     __syncthreads();
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -181,17 +194,18 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
   for (int64_t r0 = ((int64_t)blockIdx.x * nw + warp) * 8; r0 < m; r0 += (int64_t)gridDim.x * nw * 8) {
     const int64_t row = r0 + (lane >> 2);
     const bool row_ok = row < m;
-    // opaque per-iteration copies of the smem bases: stops the compiler from hoisting the
-    // (loop-invariant) R fragment loads out of the row loop into hundreds of registers
+    // opaque per-iteration copies: stop the compiler from hoisting loop-invariant R loads and
+    // per-column offsets/predicates out of the row loop into hundreds of registers
     const double* Rt = Rt_base;
     const double* Rd = Rd_base;
-    int64_t ldz_l = ldz, ldq_l = ldq;  // likewise the per-column offsets col*ldz, col*ldq
-    int n_l = n;                       // and the per-column predicates col < n
-    asm volatile("" : "+l"(Rt), "+l"(Rd), "+l"(ldz_l), "+l"(ldq_l), "+r"(n_l));
+    const double* Ri = Ri_base;
+    int64_t ldz_l = ldz, ldq_l = ldq;
+    int n_l = n;
+    const double* Rg = R;
+    asm volatile("" : "+l"(Rt), "+l"(Rd), "+l"(Ri), "+l"(ldz_l), "+l"(ldq_l), "+r"(n_l), "+l"(Rg));
     double qa[NT][2];                     // A fragments: Q[r0 + lane/4, jt*8 + 4h + lane%4]
     // Z of tile jt+1 is loaded before tile jt's Q stores: different columns, so this is safe
-    // even in place (Q == Z), and it takes the global-load latency off the per-tile chain
-    // (the compiler must assume Q aliases Z and would not reorder these itself).
+    // even in place (Q == Z); the compiler must assume Q aliases Z and would not reorder these.
     double znext[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -208,69 +222,47 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
           znext[e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
         }
       }
-      // off-diagonal partial sums on DMMA (two accumulators: independent chains)
-      double s0[2] = {0.0, 0.0}, s1[2] = {0.0, 0.0};
-      const int bcol = jt * 8 + (lane >> 2);
-      const double* rb = R + (int64_t)(bcol < n ? bcol : 0) * ldr + q4;
+      // off-diagonal partial sums on DMMA (four independent accumulator chains)
+      double sacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int kt = 0; kt < jt; ++kt) {
-        double b0, b1;
-        if (SMEM_R) {
-          const double* f = Rt + (size_t)(jt * (jt - 1) / 2 + kt) * 64 + lane;
-          b0 = f[0];
-          b1 = f[32];
-        } else {
-          b0 = bcol < n ? rb[kt * 8] : 0.0;
-          b1 = bcol < n ? rb[kt * 8 + 4] : 0.0;
-        }
-        if (kt & 1) {
-          dmma_f(s1, qa[kt][0], b0);
-          dmma_f(s1, qa[kt][1], b1);
-        } else {
-          dmma_f(s0, qa[kt][0], b0);
-          dmma_f(s0, qa[kt][1], b1);
-        }
+        const double* f = Rt + (size_t)(jt * (jt - 1) / 2 + kt) * 64 + lane;
+        const double b0 = f[0], b1 = f[32];
+        dmma_f(sacc[kt & 3], qa[kt][0], b0);
+        dmma_f(sacc[kt & 3], qa[kt][1], b1);
       }
-      // t = z - s for this lane's two entries (row, jt*8 + 2*q4 + e)
-      double t[2];
-      t[0] = zc0 - (s0[0] + s1[0]);
-      t[1] = zc1 - (s0[1] + s1[1]);
-      // diagonal 8 x 8 block by substitution
-      double qc[2] = {0.0, 0.0};
+      double t0 = zc0 - ((sacc[0][0] + sacc[1][0]) + (sacc[2][0] + sacc[3][0]));
+      double t1 = zc1 - ((sacc[0][1] + sacc[1][1]) + (sacc[2][1] + sacc[3][1]));
+      // gather the row's 8 values into every lane of its quad
+      double tt[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        tt[2 * q] = __shfl_sync(0xffffffffu, t0, gbase | q);
+        tt[2 * q + 1] = __shfl_sync(0xffffffffu, t1, gbase | q);
+      }
+      // diagonal 8 x 8 block: right-looking substitution, redundantly in the 4 lanes of the quad
+      double qv[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int dc = jt * 8 + c;
-        double rcc;
-        if (SMEM_R) rcc = Rd[(jt * 8 + c) * 8 + c];
-        else rcc = dc < n ? R[(int64_t)dc * ldr + dc] : 1.0;
-        const double mine = t[c & 1] / rcc;  // meaningful in the owner lane (q4 == c/2)
-        const double qv = __shfl_sync(0xffffffffu, mine, gbase | (c >> 1));
-        if (q4 == (c >> 1)) qc[c & 1] = qv;
+        qv[c] = tt[c] * Ri[dc];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = 2 * q4 + e;
-          if (col > c) {
-            const int gc = jt * 8 + col;
-            double rcj;
-            if (SMEM_R) rcj = Rd[(jt * 8 + c) * 8 + col];
-            else rcj = gc < n ? R[(int64_t)gc * ldr + dc] : 0.0;
-            t[e] -= qv * rcj;
-          }
+        for (int c2 = c + 1; c2 < 8; ++c2) {
+          double rcj;
+          if (SMEM_RD) rcj = Rd[(jt * 8 + c) * 8 + c2];
+          else rcj = (jt * 8 + c2) < n_l ? Rg[(int64_t)(jt * 8 + c2) * ldr + dc] : 0.0;
+          tt[c2] = fma(-qv[c], rcj, tt[c2]);
         }
       }
+      // this lane's two C entries -> Q, and the tile's A fragments (row lane/4, cols 4h + lane%4)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = jt * 8 + 2 * q4 + e;
-        if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qc[e];
+        const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+        if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
       }
-      // C layout -> A fragments of this tile: qa[jt][h] = q(row, jt*8 + 4h + lane%4)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int src = gbase | (2 * h + (q4 >> 1));
-        const double v0 = __shfl_sync(0xffffffffu, qc[0], src);
-        const double v1 = __shfl_sync(0xffffffffu, qc[1], src);
-        qa[jt][h] = (lane & 1) ? v1 : v0;
-      }
+      qa[jt][0] = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
+      qa[jt][1] = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
     }
   }
 }
@@ -285,11 +277,12 @@ static int trsm_num_sms() {
 template <int NT>
 static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
                            double* Q, int64_t ldq, const int* info, cudaStream_t s) {
-  constexpr size_t bytes = trsm_smem_doubles<NT>() * sizeof(double);
-  constexpr bool smem_r = bytes <= (size_t)SMEM_MAX;
+  constexpr bool smem_rd = trsm_smem_doubles<NT>(true) * sizeof(double) <= (size_t)SMEM_MAX;
+  constexpr size_t bytes = trsm_smem_doubles<NT>(smem_rd) * sizeof(double);
+  static_assert(bytes <= (size_t)SMEM_MAX, "R fragments must fit in shared memory");
   static bool attr_done = false;
-  if (smem_r && !attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(trsm_dmma_kernel<NT, smem_r>,
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(trsm_dmma_kernel<NT, smem_rd>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
@@ -297,7 +290,7 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   int64_t g = cdiv(m, (TRSM_THREADS / 32) * 8);  // 8 rows per warp per pass
   const int sms = trsm_num_sms();
   if (g > sms) g = sms;          // persistent: R is staged once per CTA
-  trsm_dmma_kernel<NT, smem_r><<<(unsigned)g, TRSM_THREADS, smem_r ? bytes : 0, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
+  trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, TRSM_THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
   return cudaSuccess;
 }
 

@@ -9,8 +9,36 @@ import torch  # noqa: E402
 import gen  # noqa: E402
 import paper_1401_5171_b200 as oqr  # noqa: E402
 
-cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+cfg = sys.argv[1] if len(sys.argv) > 1 else "3"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+if cfg in gen.TRIDIAG_CONFIGS:
+    d, e, p = gen.tridiag_config(cfg)
+    m, n = p.m, p.n
+    dg, eg = torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda()
+    Z = torch.from_numpy(p.Z).cuda()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    G = oqr.gram_tridiag(dg, eg, Z)
+    R, info = oqr.potrf(G)
+    res = {"gram_tridiag (pack Z, pack TZ, K4', K1r)": timed(lambda: oqr.gram_tridiag(dg, eg, Z, G)),
+           "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)), "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
+    for v in ("normal", "normal2", "prequr"):
+        res[v] = timed(lambda: oqr.VARIANTS_TRIDIAG[v](dg, eg, Z))
+    fl = 2.0 * m * n * n
+    print(f"tridiag config {cfg} m={m} n={n}: " + ", ".join(f"{k} {v:.4f} ms" for k, v in res.items()) +
+          f"; normal {fl / res['normal'] / 1e9:.2f} TFLOP/s (2mn^2 normalisation)")
+    sys.exit(0)
+cfg = int(cfg)
 p = gen.config(cfg)
 m, n = p.m, p.n
 A = torch.from_numpy(p.A).cuda()
@@ -43,4 +71,4 @@ for v in ("normal", "normal2", "prequr"):
     res[v] = timed(lambda: oqr.VARIANTS[v](A, Z, Q, Rv))
 fl = 2.0 * m * m * n + 2.0 * m * n * n
 print(f"config {cfg} m={m} n={n}: " + ", ".join(f"{k} {v:.4f} ms" for k, v in res.items()) +
-      f"; normal {fl / res['normal'] / 1e9:.1f} GFLOP/s")
+      f"; normal {fl / res['normal'] / 1e9:.1f} TFLOP/s")
