@@ -83,6 +83,24 @@ int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double*
                double* Q, double* R, oqr_stream_t stream);
 
 /*
+ * Symmetric-A variants.  A is SPD, hence symmetric: these read
+ * only the block-lower triangle of A (64 x 64 blocks: A[i, j] for floor(j/64) <= floor(i/64))
+ * -- half the bytes and half the flops of the dense calls.  With A = L + D + L^T by blocks,
+ * G = Z^T A Z = T + T^T where T = sum_I Z_I^T (sum_{J<I} A_IJ Z_J + (1/2) A_II Z_I); the 1/2 is
+ * applied exactly to Z.  G is bitwise symmetric.  Same arguments, outputs and status codes as
+ * the dense calls; for an A that is not symmetric they factor the block-lower symmetrisation.
+ */
+int oqr_normal_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                   double* Q, double* R, oqr_stream_t stream);
+int oqr_normal2_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                    double* Q, double* R, oqr_stream_t stream);
+int oqr_prequr_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                   double* Q, double* R, oqr_stream_t stream);
+/* Step export of the symmetric Gram (asynchronous). */
+int oqr_gram_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* G,
+                 oqr_stream_t stream);
+
+/*
  * Tridiagonal A (the paper's second workload):
  * A = tridiag(e, d, e) symmetric positive definite, d: m diagonal entries, e: m-1 off-diagonal
  * entries (device pointers; e may be NULL when m == 1).  Same algorithms, outputs and status

@@ -24,7 +24,8 @@ __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm"
            "launch_count", "EXPORTS"]
 
 # Every symbol include/oqr.h declares.
-EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_tridiag", "oqr_normal2_tridiag",
+EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
+           "oqr_gram_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
            "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_gram_rows", "oqr_sum_partials",
            "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_launch_count")
@@ -48,7 +49,8 @@ def lib() -> ctypes.CDLL:
                                "`python -c 'import __graft_entry__ as g; g.build()'`")
         L = ctypes.CDLL(LIB_PATH)
         I64, P, I = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
-        for name in ("oqr_normal", "oqr_normal2", "oqr_prequr"):
+        for name in ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_sym", "oqr_normal2_sym",
+                     "oqr_prequr_sym"):
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, I64, P, I64, P, P, P]
@@ -60,6 +62,8 @@ def lib() -> ctypes.CDLL:
         L.oqr_gram_tridiag.argtypes = [I64, I64, P, P, P, I64, P, P]
         L.oqr_status_string.restype = ctypes.c_char_p
         L.oqr_status_string.argtypes = [I]
+        L.oqr_gram_sym.restype = I
+        L.oqr_gram_sym.argtypes = [I64, I64, P, I64, P, I64, P, P]
         L.oqr_gram.restype = I
         L.oqr_gram.argtypes = [I64, I64, P, I64, P, I64, P, P]
         L.oqr_gram_euclid.restype = I
@@ -144,6 +148,35 @@ def prequr(A, Z, Q=None, R=None, stream=None, check: bool = True):
 
 
 VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr}
+
+
+def normal_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    """CHOLQR reading only the block-lower triangle of the (symmetric) A (NEXT-N4)."""
+    return _variant("oqr_normal_sym", A, Z, Q, R, stream, check)
+
+
+def normal2_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant("oqr_normal2_sym", A, Z, Q, R, stream, check)
+
+
+def prequr_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant("oqr_prequr_sym", A, Z, Q, R, stream, check)
+
+
+VARIANTS_SYM = {"normal": normal_sym, "normal2": normal2_sym, "prequr": prequr_sym}
+
+
+def gram_sym(A, Z, G=None, stream=None):
+    """Symmetric Gram G = T + T^T from the block-lower triangle of A (asynchronous step export)."""
+    import torch
+    m, n = A.shape[0], Z.shape[0]
+    if G is None:
+        G = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    st = lib().oqr_gram_sym(m, n, _check(A, "A", m), A.shape[1], _check(Z, "Z", m), Z.shape[1],
+                            _check(G, "G", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_gram_sym")
+    return G
 
 
 def _vec(t, name: str, length: int):

@@ -130,6 +130,7 @@ struct AOp {
   const double* d = nullptr;
   const double* e = nullptr;
   bool tridiag = false;
+  bool sym = false;  // dense A read as symmetric: block-lower triangle only (NEXT-N4)
 };
 
 // G (ld n) = Z^T A Z through the packed copy of Z held in ws.Zp (and, for tridiagonal A, the
@@ -141,10 +142,13 @@ static int gram_into(const AOp& op, int64_t m, int n, const double* Z, int64_t l
   if (op.tridiag) {
     OQR_TRY(launch_pack_w_tridiag(m, n, op.d, op.e, Z, ldz, ws.Zc, s));
     OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zc, ws.P, &g, s));
+  } else if (op.sym) {
+    OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zc, s, 0.5));  // Z / 2 (exact) for the diagonal panels
+    OQR_TRY(launch_gram_fused(m, m, n, op.A, op.lda, ws.Zp, ws.Zp, ws.Zc, ws.P, &g, s));
   } else {
-    OQR_TRY(launch_gram_fused(m, m, n, op.A, op.lda, ws.Zp, ws.Zp, ws.P, &g, s));
+    OQR_TRY(launch_gram_fused(m, m, n, op.A, op.lda, ws.Zp, ws.Zp, nullptr, ws.P, &g, s));
   }
-  OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s));
+  OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s, op.sym));
   return 0;
 }
 
@@ -184,7 +188,7 @@ namespace oqr {
 static int run_normal(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
                       cudaStream_t s) {
   Workspace ws;
-  int st = ws.alloc(m, n, s, op.tridiag ? m : 0);
+  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
   if (st) return st;
   if ((st = cholqr_pass(op, m, n, Z, ldz, Q, R, 0, ws, s))) return st;
   return finish(ws, s);
@@ -193,7 +197,7 @@ static int run_normal(const AOp& op, int64_t m, int n, const double* Z, int64_t 
 static int run_normal2(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
                        cudaStream_t s) {
   Workspace ws;
-  int st = ws.alloc(m, n, s, op.tridiag ? m : 0);
+  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
   if (st) return st;
   // pass 1: [Q1, R1] = CHOLQR(A, Z), Q1 into Q
   if ((st = cholqr_pass(op, m, n, Z, ldz, Q, ws.R1, 0, ws, s))) return st;
@@ -207,7 +211,7 @@ static int run_normal2(const AOp& op, int64_t m, int n, const double* Z, int64_t
 static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
                       cudaStream_t s) {
   Workspace ws;
-  int st = ws.alloc(m, n, s, op.tridiag ? m : 0);
+  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
   if (st) return st;
   // pre-step: S = chol(Z^T Z), Y = Z S^{-1} (into Q)
   if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
@@ -220,10 +224,11 @@ static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t 
   return finish(ws, s);
 }
 
-static AOp dense_op(const double* A, int64_t lda) {
+static AOp dense_op(const double* A, int64_t lda, bool sym = false) {
   AOp op;
   op.A = A;
   op.lda = lda;
+  op.sym = sym;
   return op;
 }
 
@@ -273,6 +278,38 @@ int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double*
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
   return run_prequr(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_normal_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                   double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  return run_normal(dense_op(A, lda, true), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_normal2_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                    double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  return run_normal2(dense_op(A, lda, true), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_prequr_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                   double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  return run_prequr(dense_op(A, lda, true), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_gram_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* G,
+                 oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, nullptr, nullptr, true, false);
+  if (st) return st;
+  if (G == nullptr) return -7;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws;
+  if ((st = ws.alloc(m, (int)n, s, m))) return st;
+  return gram_into(dense_op(A, lda, true), m, (int)n, Z, ldz, G, ws, s);
 }
 
 int oqr_normal_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
@@ -355,7 +392,7 @@ int oqr_gram_rows(int64_t m, int64_t n, int64_t r0, int64_t mr, const double* Ar
   int g = 0;
   OQR_TRY(launch_pack_z(m, ni, Z, ldz, ws.Zp, s));
   OQR_TRY(launch_pack_z(mr, ni, Z + r0, ldz, ws.Zc, s));
-  OQR_TRY(launch_gram_fused(m, mr, ni, Ar, ldar, ws.Zp, ws.Zc, ws.P, &g, s));
+  OQR_TRY(launch_gram_fused(m, mr, ni, Ar, ldar, ws.Zp, ws.Zc, nullptr, ws.P, &g, s));
   OQR_TRY(launch_gram_reduce(ni, g, ws.P, G, ni, s));
   return 0;
 }

@@ -103,7 +103,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 // ------------------------------------------------------------------ Z packing -------------
 // Zp[((b*NT + lt)*4 + kk)*32 + ln] = Z[b*BK + kk*4 + ln%4, lt*8 + ln/4] (zero outside Z).
 __global__ void pack_z_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t ldz,
-                              double* __restrict__ Zp, int64_t total) {
+                              double* __restrict__ Zp, int64_t total, double scale) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int ln = (int)(e & 31);
@@ -115,17 +115,17 @@ __global__ void pack_z_kernel(int64_t m, int n, int NT, const double* __restrict
     const int64_t row = b * BK + kk * 4 + (ln & 3);
     const int col = lt * 8 + (ln >> 2);
     double v = 0.0;
-    if (row < m && col < n) v = Z[(int64_t)col * ldz + row];
+    if (row < m && col < n) v = scale * Z[(int64_t)col * ldz + row];  // scale: 1 or 1/2 (exact)
     Zp[e] = v;
   }
 }
 
-cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s) {
+cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s, double scale) {
   const int NT = (int)cdiv(n, 8);
   const int64_t total = zp_doubles(m, 8 * NT);
   int64_t blocks = cdiv(total, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  pack_z_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, n, NT, Z, ldz, Zp, total);
+  pack_z_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, n, NT, Z, ldz, Zp, total, scale);
   note_launch();
   return cudaGetLastError();
 }
@@ -242,21 +242,74 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
 }
 
 // ------------------------------------------------------------------ K1 --------------------
+// Unit schedule.  Dense: every panel I has KB k-blocks.  SYM (NEXT-N4, symmetric A): panel I only
+// has the k-blocks of the block-lower triangle including its own 64 x 64 diagonal panel,
+// nk(I) = min(KB, 4 (I + 1)), so the units before panel I number 2 I (I + 1) (only the last
+// panel can be clipped).
+template <bool SYM>
+__host__ __device__ __forceinline__ int unit_nk(int I, int KB) {
+  return SYM ? min(KB, (I + 1) * (BM / BK)) : KB;
+}
+// Balanced split of the unit range over the CTAs: a panel costs its units plus one contraction
+// (~PANEL_W units of DMMA time), so the split equalises W(u) = u + PANEL_W * (panels started
+// before u) instead of u alone -- the symmetric schedule has panels of 4 .. KB units.
+constexpr int PANEL_W = 24;
+
+template <bool SYM>
+__host__ __device__ __forceinline__ int unit_panels_before(int u, int KB) {  // panels starting at < u
+  if (u <= 0) return 0;
+  if (!SYM) return (u + KB - 1) / KB;
+  int i = (int)((sqrt(2.0 * (double)u + 1.0) - 1.0) * 0.5);
+  while (2LL * (i + 1) * (i + 2) < (long long)u) ++i;     // largest i with start(i) = 2i(i+1) < u
+  while (i > 0 && 2LL * i * (i + 1) >= (long long)u) --i;
+  return i + 1;
+}
+
+template <bool SYM>
+__device__ __forceinline__ int unit_split(int c, int g, int U, int KB, int npanels) {
+  if (c <= 0) return 0;
+  if (c >= g) return U;
+  const double target = ((double)U + (double)PANEL_W * npanels) * c / g;
+  int lo = 0, hi = U;  // smallest u with W(u) >= target
+  while (lo < hi) {
+    const int mid = lo + (hi - lo) / 2;
+    if ((double)mid + (double)PANEL_W * unit_panels_before<SYM>(mid, KB) >= target) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+template <bool SYM>
+__host__ __device__ __forceinline__ void unit_locate(int u, int KB, int* I, int* kb) {
+  if (!SYM) {
+    *I = u / KB;
+    *kb = u - *I * KB;
+    return;
+  }
+  int i = (int)((sqrt(2.0 * (double)u + 1.0) - 1.0) * 0.5);
+  while (2LL * (i + 1) * (i + 2) <= (long long)u) ++i;
+  while (i > 0 && 2LL * i * (i + 1) > (long long)u) --i;
+  *I = i;
+  *kb = u - 2 * i * (i + 1);
+}
+
 // Fill a ring slot with unit (panel I, k-block kb): the A tile A[I*BM.., kb*BK..] (64 x 16,
 // column-major in smem, 8 KiB) and the packed Z block kb (NT KiB).  Executed by warp 0's lanes.
 // With a tensor map (A 16-byte aligned, lda even) both are single async requests and ragged
 // tiles need nothing special: TMA zero-fills rows/columns >= m.  Otherwise the A tile is loaded
 // with plain loads and zero fill (correct, slow).
-template <int NT>
+template <int NT, bool SYM>
 __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr, const CUtensorMap* tmap,
                                             const double* __restrict__ A, int64_t lda,
-                                            const double* __restrict__ Zp, double* As, uint64_t* bar,
-                                            int lane, uint64_t pol_a, uint64_t pol_z, bool tma_ok) {
+                                            const double* __restrict__ Zp, const double* __restrict__ Zh,
+                                            double* As, uint64_t* bar, int lane, uint64_t pol_a, uint64_t pol_z,
+                                            bool tma_ok) {
   constexpr uint32_t zbytes = NT * 4 * FRAG * 8;
   constexpr uint32_t abytes = BM * BK * 8;
   const int64_t row0 = (int64_t)I * BM, col0 = (int64_t)kb * BK;
   double* Zs = As + BM * BK;
-  const double* zsrc = Zp + kb * (int64_t)(NT * 4 * FRAG);
+  // SYM: the diagonal panel's k-blocks (kb >= 4 I) use Z / 2 (exact), so T = S + D/2 and G = T + T^T
+  const double* zsrc = ((SYM && kb >= I * (BM / BK)) ? Zh : Zp) + kb * (int64_t)(NT * 4 * FRAG);
 #ifdef OQR_EXP_NOLOAD  // experiment build only (tools/exp): no copies, barrier still completes
   if (lane == 0) mbar_arrive(bar);
   __syncwarp();
@@ -289,11 +342,11 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr
 // NTW for the first column half, NT - NTW for the second (one less when NT is odd), so no
 // DMMA is predicated.  Unit bookkeeping is incremental int32 (no division in the loop):
 // (I, kb) is the unit being consumed, (Ii, kbi) the unit `stages` ahead that a refill loads.
-template <int NT, int NTL>
+template <int NT, int NTL, bool SYM>
 __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m, int64_t mr,
                                               const double* __restrict__ A, int64_t lda,
                                               const double* __restrict__ Zp, const double* __restrict__ Zc,
-                                              double* slot,
+                                              const double* __restrict__ Zh, double* slot,
                                               double* red, double* ring, uint64_t* full, uint64_t* empty,
                                               unsigned* relcnt, int KB, int u0, int u1, int stages,
                                               bool tma_ok, int rg, int ch, int lane, uint64_t pol_a,
@@ -307,9 +360,13 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
   bool first = true;
   int s = 0;
   uint32_t ph = 0;
-  int I = u0 / KB, kb = u0 - I * KB;
+  int I, kb;
+  unit_locate<SYM>(u0, KB, &I, &kb);
+  int nk = unit_nk<SYM>(I, KB);
   int ui = u0 + stages;  // next unit to be loaded into the slot being released
-  int Ii = ui / KB, kbi = ui - Ii * KB;
+  int Ii, kbi;
+  unit_locate<SYM>(ui, KB, &Ii, &kbi);
+  int nki = unit_nk<SYM>(Ii, KB);
   // A fragment: A[row0 + rg*8 + lane/4, col0 + kk*4 + lane%4] from the column-major 64 x 16 tile
   const int a_off = (lane & 3) * BM + rg * 8 + (lane >> 2);
   // B fragment (lt, kk): 32 consecutive doubles of the packed block
@@ -350,18 +407,20 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last && ui < u1) {
       mbar_wait(&empty[s], ph);
-      issue_stage<NT>(Ii, kbi, m, mr, tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z, tma_ok);
+      issue_stage<NT, SYM>(Ii, kbi, m, mr, tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
+                           tma_ok);
     }
     ++ui;
-    if (++kbi == KB) {
+    if (++kbi == nki) {
       kbi = 0;
       ++Ii;
+      nki = unit_nk<SYM>(Ii, KB);
     }
     if (++s == stages) {
       s = 0;
       ph ^= 1;
     }
-    const bool panel_end = (++kb == KB);
+    const bool panel_end = (++kb == nk);
     if (panel_end || u + 1 == u1) {
       contract_panel<NT>(acc, (int64_t)I * BM, Zc, red, slot, first, rg, ch, lane, threadIdx.x);
       first = false;
@@ -371,6 +430,7 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     if (panel_end) {
       kb = 0;
       ++I;
+      nk = unit_nk<SYM>(I, KB);
     }
   }
 }
@@ -380,11 +440,11 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
 // operand fragments of k-step kk+1 are loaded while the DMMAs of k-step kk run.  Warp 0 fills
 // the ring initially; afterwards whichever warp releases slot s last refills it with the unit
 // `stages` ahead, so `stages - 1` stages of compute cover the copy latency.
-template <int NT>
+template <int NT, bool SYM>
 __global__ void __launch_bounds__(NCW * 32, 1)
 gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t mr, const double* __restrict__ A,
                   int64_t lda, const double* __restrict__ Zp, const double* __restrict__ Zc,
-                  double* __restrict__ P, int KB, int U, int stages, bool tma_ok) {
+                  const double* __restrict__ Zh, double* __restrict__ P, int KB, int U, int stages, bool tma_ok) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
   constexpr int STAGE = BM * BK + NT * 4 * FRAG;  // doubles per pipeline stage
@@ -398,7 +458,13 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rg = warp % NRG, ch = warp / NRG;
   const int g = gridDim.x, c = blockIdx.x;
-  const int u0 = (int)((int64_t)U * c / g), u1 = (int)((int64_t)U * (c + 1) / g);
+  const int npanels = (int)cdiv(mr, BM);
+  const int u0 = unit_split<SYM>(c, g, U, KB, npanels), u1 = unit_split<SYM>(c + 1, g, U, KB, npanels);
+  if (u0 >= u1) {  // the weighted split can leave a CTA without units: its slot is zero
+    double* slot = P + c * (int64_t)NP * NP;
+    for (int e = threadIdx.x; e < NP * NP; e += blockDim.x) slot[e] = 0.0;
+    return;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -415,18 +481,19 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
   const uint64_t pol_z = policy_evict_last();   // Zp is re-read by every panel
   if (warp == 0) {
     for (int s = 0; s < stages && u0 + s < u1; ++s) {
-      const int u = u0 + s, I = u / KB;
-      issue_stage<NT>(I, u - I * KB, m, mr, &tmap, A, lda, Zp, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
-                      tma_ok);
+      int I, kb;
+      unit_locate<SYM>(u0 + s, KB, &I, &kb);
+      issue_stage<NT, SYM>(I, kb, m, mr, &tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
+                           tma_ok);
     }
   }
   double* slot = P + c * (int64_t)NP * NP;
   if (ch == 0)
-    consume_units<NT, NTW>(&tmap, m, mr, A, lda, Zp, Zc, slot, red, ring, full, empty, relcnt, KB, u0, u1,
-                           stages, tma_ok, rg, ch, lane, pol_a, pol_z);
-  else
-    consume_units<NT, NT - NTW>(&tmap, m, mr, A, lda, Zp, Zc, slot, red, ring, full, empty, relcnt, KB, u0,
+    consume_units<NT, NTW, SYM>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB, u0,
                                 u1, stages, tma_ok, rg, ch, lane, pol_a, pol_z);
+  else
+    consume_units<NT, NT - NTW, SYM>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB,
+                                     u0, u1, stages, tma_ok, rg, ch, lane, pol_a, pol_z);
 }
 
 // ------------------------------------------------------------------ K4' -------------------
@@ -559,29 +626,36 @@ gram_packed_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp,
 
 // ------------------------------------------------------------------ K1r -------------------
 // G[k, l] = sum_{c=0}^{g-1} P[c][l*NP + k], c ascending (fixed order => reproducible bits).
+// sym (NEXT-N4): G = T + T^T with T = sum_c P[c], i.e. G[k,l] = T[k,l] + T[l,k] (bitwise symmetric).
 __global__ void gram_reduce_kernel(int n, int NP, int g, const double* __restrict__ P,
-                                   double* __restrict__ G, int64_t ldg) {
+                                   double* __restrict__ G, int64_t ldg, bool sym) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
   const int l = (int)(idx / n), k = (int)(idx - (int64_t)l * n);
-  const double* p = P + (int64_t)l * NP + k;
   const int64_t stride = (int64_t)NP * NP;
+  const double* p = P + (int64_t)l * NP + k;
   double s = p[0];
   for (int c = 1; c < g; ++c) s += p[c * stride];
+  if (sym) {
+    const double* q = P + (int64_t)k * NP + l;
+    double t = q[0];
+    for (int c = 1; c < g; ++c) t += q[c * stride];
+    s = (k <= l) ? s + t : t + s;  // same operand order for (k,l) and (l,k)
+  }
   G[(int64_t)l * ldg + k] = s;
 }
 
-cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s) {
+cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s, bool sym) {
   const int NP = 8 * (int)cdiv(n, 8);
   const int64_t total = (int64_t)n * n;
-  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, NP, g, P, G, ldg);
+  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, NP, g, P, G, ldg, sym);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s) {
   const int64_t total = (int64_t)n * n;
-  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, n, count, P, G, ldg);
+  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, n, count, P, G, ldg, false);
   note_launch();
   return cudaGetLastError();
 }
@@ -643,19 +717,21 @@ static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t mr, int64_t m
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NT>
+template <int NT, bool SYM>
 static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t lda, const double* Zp,
-                                 const double* Zc, double* P, int* g_out, cudaStream_t s) {
+                                 const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s) {
   size_t bytes;
   const int stages = fused_stages(NT, &bytes);
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gram_fused_kernel<NT>,
+    cudaError_t e = cudaFuncSetAttribute(gram_fused_kernel<NT, SYM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int64_t KB = cdiv(m, BK), U = cdiv(mr, BM) * KB;  // U < 2^31 for every m that fits in HBM
+  const int64_t KB = cdiv(m, BK), NPAN = cdiv(mr, BM);
+  // U < 2^31 for every m that fits in HBM.  SYM: 2 P (P - 1) units before the last panel.
+  const int64_t U = SYM ? 2 * (NPAN - 1) * NPAN + unit_nk<true>((int)(NPAN - 1), (int)KB) : NPAN * KB;
   if (U > (int64_t)INT32_MAX - 64) return cudaErrorInvalidValue;
   int64_t g = num_sms();
   if (g > U) g = U;
@@ -664,8 +740,8 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
   std::memset(&tmap, 0, sizeof(tmap));
   const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda);
   timing_begin(s);
-  gram_fused_kernel<NT><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, P, (int)KB, (int)U,
-                                                             stages, tma_ok);
+  gram_fused_kernel<NT, SYM><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, Zh, P, (int)KB,
+                                                                  (int)U, stages, tma_ok);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);
@@ -702,10 +778,13 @@ static cudaError_t gram_packed_nt(int64_t m, const double* Xp, const double* Yp,
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
 
 cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int64_t lda, const double* Zp,
-                              const double* Zc, double* P, int* g_out, cudaStream_t s) {
+                              const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s) {
+  if (Zh != nullptr && mr != m) return cudaErrorInvalidValue;  // SYM is a whole-matrix schedule
   switch ((int)cdiv(n, 8)) {
-#define OQR_CASE(NT) \
-  case NT: return gram_fused_nt<NT>(m, mr, A, lda, Zp, Zc, P, g_out, s);
+#define OQR_CASE(NT)                                                                        \
+  case NT:                                                                                  \
+    return Zh ? gram_fused_nt<NT, true>(m, mr, A, lda, Zp, Zc, Zh, P, g_out, s)              \
+              : gram_fused_nt<NT, false>(m, mr, A, lda, Zp, Zc, nullptr, P, g_out, s);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

@@ -41,15 +41,18 @@ void timing_end(cudaStream_t s);
 
 // ---- launchers (return cudaError_t of the launch) ----
 // Z (m x n, ldz) -> Zp (packed, NP = 8*ceil(n/8) columns)
-cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s);
+cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s,
+                          double scale = 1.0);
 // Per-CTA partial Gram slots P[g][NP][NP] of Z^T (A Z); returns the grid size used in *g_out.
 // A is moved by 2-D tensor TMA when it is 16-byte aligned with an even lda; otherwise by plain
 // loads (same results, slow).
 // Rows [0, mr) of A (or of a row block of A holding mr rows, all m columns): slots of
 // Z_rows^T (A_rows Z) where Zp packs all m rows of Z (B operand) and Zc packs the mr rows of Z
-// that match the A rows (contraction operand; Zc == Zp on one GPU).
+// that match the A rows (contraction operand; Zc == Zp on one GPU).  Zh != nullptr selects the
+// symmetric schedule (NEXT-N4; mr == m): only the block-lower triangle of A is read, Zh = Z/2
+// packed, and the slots hold T with G = T + T^T (launch_gram_reduce(..., sym = true)).
 cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int64_t lda, const double* Zp,
-                              const double* Zc, double* P, int* g_out, cudaStream_t s);
+                              const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s);
 // G (n x n, ldg) = sum_{c<count} P_c, P_c = n x n (ld n) consecutive, c ascending.
 cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s);
 // W = T Z (T = tridiag(e, d, e)) packed like Zp.
@@ -59,7 +62,8 @@ cudaError_t launch_pack_w_tridiag(int64_t m, int n, const double* d, const doubl
 cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
                                cudaStream_t s);
 // G (n x n, ldg) = sum_{c<g} P[c] in fixed c order.
-cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s);
+cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s,
+                               bool sym = false);
 // R = chol(G) (upper); *info = 0 | k (info_off == 0), or (only if *info == 0) n + k.
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
                          int info_off, cudaStream_t s);

@@ -56,7 +56,7 @@ def test_sass_uses_fp64_tensor_pipe_and_bulk_copy(L):
     import paper_1401_5171_b200 as oqr
     syms = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-symbols", oqr.LIB_PATH],
                           capture_output=True, text=True).stdout
-    name = re.search(r"(_ZN3oqr17gram_fused_kernelILi25EE\w+)", syms).group(1)
+    name = re.search(r"(_ZN3oqr17gram_fused_kernelILi25ELb0EE\w+)", syms).group(1)
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun", name, oqr.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "DMMA" in out            # mma.sync f64 -> FP64 tensor pipe

@@ -198,9 +198,10 @@ def outcome_determined(p, variant):
     return ok
 
 
-def variant_gates(oqr, p, variant):
+def variant_gates(oqr, p, variant, family="dense"):
     m, n = p.m, p.n
-    Q, R, st = oqr.VARIANTS[variant](to_dev(p.A), to_dev(p.Z))
+    fams = {"dense": oqr.VARIANTS, "sym": oqr.VARIANTS_SYM}
+    Q, R, st = fams[family][variant](to_dev(p.A), to_dev(p.Z))
     Qo, Ro, sto = oracle.VARIANTS[variant](p.A, p.Z, m)
     cls = lambda s: 0 if s == 0 else (1 if s <= n else 2)
     if outcome_determined(p, variant):                          # T7
@@ -307,3 +308,43 @@ def test_stream_and_launch_accounting(oqr):
         assert oqr.launch_count() - n0 == 5          # pack, K1, K1r, K2, K3
     Qo, Ro, _ = oracle.normal(p.A, p.Z, p.m)
     assert np.linalg.norm(host(R) - Ro) / np.linalg.norm(Ro) < 1e-12
+
+
+# ---------------------------------------------------- NEXT-N4: symmetric A (block-lower triangle)
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_t1_gram_sym(oqr, shape):
+    p = make(*shape)
+    m, n = p.m, p.n
+    G = host(oqr.gram_sym(to_dev(p.A), to_dev(p.Z)))
+    assert np.array_equal(G, G.T)                                   # bitwise symmetric by construction
+    Gd, M = oracle.dd_gram(p.A, p.Z, m)
+    Go = oracle.from_cm(oracle.gram(p.A, p.Z, m), n)
+    assert np.all(np.abs(G.T - Go) <= 2 * gamma(3 * m) * M)
+    assert np.all(np.abs(G.T - Gd) <= gamma(3 * m) * M)
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_variants_sym(oqr, shape, variant):
+    variant_gates(oqr, make(*shape), variant, family="sym")
+
+
+def test_sym_reads_only_block_lower_triangle(oqr):
+    # poisoning the strictly block-upper part of A must not change the result
+    p = make(300, 20, 1e3, 1e2, 17)
+    A = p.A.copy()                  # storage (cols, rows): A[j, i] is element (i, j)
+    for j in range(300):
+        for i in range(300):
+            if j // 64 > i // 64:   # block column beyond the row's block: upper, never read
+                A[j, i] = np.nan
+    Q1, R1, s1 = oqr.normal_sym(to_dev(p.A), to_dev(p.Z))
+    Q2, R2, s2 = oqr.normal_sym(to_dev(A), to_dev(p.Z))
+    assert s1 == s2 == 0
+    assert torch.equal(R1, R2) and torch.equal(Q1, Q2)
+
+
+def test_sym_determinism(oqr):
+    p = make(4000, 50, 1e4, 1e3, 99)
+    A, Z = to_dev(p.A), to_dev(p.Z)
+    G1, G2 = oqr.gram_sym(A, Z), oqr.gram_sym(A, Z)
+    assert torch.equal(G1, G2)
