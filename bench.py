@@ -193,6 +193,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sym", action="store_true",
+                    help="NEXT-N4 symmetric family: block-lower triangle of A only (own roofline)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded code path even at N = 1 (it is the default for N > 1)")
     args = ap.parse_args()
@@ -225,7 +227,7 @@ def main():
         p = gen.config(args.config, A_out=A_h.numpy(), Z_out=Z_h.numpy())
         r0, mr = 0, m
         Q_h = pinned((n, m))
-        fn = oqr.VARIANTS[args.variant]
+        fn = (oqr.VARIANTS_SYM if args.sym else oqr.VARIANTS)[args.variant]
         Q = torch.empty((n, m), dtype=torch.float64, device=dev)
         R = torch.empty((n, n), dtype=torch.float64, device=dev)
 
@@ -246,6 +248,8 @@ def main():
         def step(A, Z):
             return normal_rows(A, Z, r0, mr)
     fl_gram = 2.0 * mr * m * n  # per K1 launch on this rank
+    if args.sym:  # block-lower triangle incl. the 64 x 64 diagonal panels
+        fl_gram = 2.0 * n * sum(min(64, m - i0) * min(m, i0 + 64) for i0 in range(0, m, 64))
     A = A_h.to(dev)
     Z = Z_h.to(dev)
     R_h = pinned((n, n))
@@ -284,11 +288,16 @@ def main():
 
     # ---- end to end through the public call with host buffers ----
     h2d = A_h.numel() * 8 + Z_h.numel() * 8
+    if args.sym:
+        h2d = sum((m - j0) * min(64, m - j0) for j0 in range(0, m, 64)) * 8 + Z_h.numel() * 8
     d2h = Q_h.numel() * 8 + R_h.numel() * 8
     barrier()
     e0.record(stream)
     for _ in range(args.e2e_steps):
-        A.copy_(A_h, non_blocking=True)
+        if args.sym:
+            oqr.upload_sym(A_h, A)      # only the block-lower triangle the *_sym calls read
+        else:
+            A.copy_(A_h, non_blocking=True)
         Z.copy_(Z_h, non_blocking=True)
         Qs, Rs, st = step(A, Z)
         Q_h.copy_(Qs, non_blocking=True)
@@ -322,14 +331,16 @@ def main():
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"configs[{args.config}] oqr_{args.variant}: m={m}, n={n}, "
+            "config": {"workload": f"configs[{args.config}] oqr_{args.variant}{'_sym' if args.sym else ''}: m={m}, n={n}, "
                                    f"kappa_A={c['kappa_a']:g}, kappa_Z={c['kappa_z']:g}",
                        "m": m, "n": n, "variant": args.variant,
                        "flops_per_step": fl, "flop_normalisation": "2m^2n+2mn^2 (PAPER.md:959-961)",
                        "l2": "inputs (A = %.1f GB) larger than L2; no flush" % (8 * m * m / 1e9),
                        "parallelism": (f"row-sharded x{world}: one n x n all-gather per step (NCCL), "
                                        "fixed rank-order sum") if (world > 1 or args.sharded) else "single GPU"},
-            "roofline": {"bound": "tensor", "kernel": "gram_fused (K1)", "achieved": achieved,
+            "roofline": {"bound": "tensor",
+                         "kernel": "gram_fused (K1)" + (" symmetric schedule: block-lower triangle" if args.sym else ""),
+                         "achieved": achieved,
                          "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,
                          "algorithmic_flops_per_launch": fl_gram, "mean_launch_ms": k1_ms,

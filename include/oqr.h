@@ -96,6 +96,13 @@ int oqr_normal2_sym(int64_t m, int64_t n, const double* A, int64_t lda, const do
                     double* Q, double* R, oqr_stream_t stream);
 int oqr_prequr_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                    double* Q, double* R, oqr_stream_t stream);
+/* Host -> device copy of exactly what the *_sym calls read: the block-lower triangle of a
+ * column-major host A (lda >= m; pinned memory for asynchrony) into A_dev (ldda >= m), one 2-D copy
+ * per 64-column panel (rows from the panel's first row to m): ~half of A's bytes.  Asynchronous on
+ * `stream`; the block-upper part of A_dev is left untouched.  Status: 0, -1 m, -2 A_host, -3 lda,
+ * -4 A_dev, -5 ldda, -100 CUDA. */
+int oqr_upload_sym(int64_t m, const double* A_host, int64_t lda, double* A_dev, int64_t ldda, oqr_stream_t stream);
+
 /* Step export of the symmetric Gram (asynchronous). */
 int oqr_gram_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* G,
                  oqr_stream_t stream);

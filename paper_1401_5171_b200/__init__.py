@@ -25,7 +25,7 @@ __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm"
 
 # Every symbol include/oqr.h declares.
 EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
-           "oqr_gram_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
+           "oqr_gram_sym", "oqr_upload_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
            "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_gram_rows", "oqr_sum_partials",
            "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_launch_count")
@@ -62,6 +62,8 @@ def lib() -> ctypes.CDLL:
         L.oqr_gram_tridiag.argtypes = [I64, I64, P, P, P, I64, P, P]
         L.oqr_status_string.restype = ctypes.c_char_p
         L.oqr_status_string.argtypes = [I]
+        L.oqr_upload_sym.restype = I
+        L.oqr_upload_sym.argtypes = [I64, P, I64, P, I64, P]
         L.oqr_gram_sym.restype = I
         L.oqr_gram_sym.argtypes = [I64, I64, P, I64, P, I64, P, P]
         L.oqr_gram.restype = I
@@ -164,6 +166,19 @@ def prequr_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
 
 
 VARIANTS_SYM = {"normal": normal_sym, "normal2": normal2_sym, "prequr": prequr_sym}
+
+
+def upload_sym(A_host, A_dev, stream=None):
+    """Copy the block-lower triangle of a (pinned) host A into A_dev: what the *_sym calls read."""
+    import torch
+    if A_host.is_cuda or A_host.dtype != torch.float64 or not A_host.is_contiguous():
+        raise TypeError("A_host: expected a contiguous float64 CPU tensor (m, lda)")
+    m = A_host.shape[0]
+    st = lib().oqr_upload_sym(m, ctypes.c_void_p(A_host.data_ptr()), A_host.shape[1], _check(A_dev, "A_dev", m),
+                              A_dev.shape[1], _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_upload_sym")
+    return A_dev
 
 
 def gram_sym(A, Z, G=None, stream=None):

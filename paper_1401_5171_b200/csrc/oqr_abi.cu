@@ -312,6 +312,21 @@ int oqr_gram_sym(int64_t m, int64_t n, const double* A, int64_t lda, const doubl
   return gram_into(dense_op(A, lda, true), m, (int)n, Z, ldz, G, ws, s);
 }
 
+int oqr_upload_sym(int64_t m, const double* A_host, int64_t lda, double* A_dev, int64_t ldda, oqr_stream_t stream) {
+  if (m < 1) return -1;
+  if (A_host == nullptr) return -2;
+  if (lda < m) return -3;
+  if (A_dev == nullptr) return -4;
+  if (ldda < m) return -5;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int64_t j0 = 0; j0 < m; j0 += BM) {  // 64-column panel: rows j0 .. m-1 (block-lower part)
+    const int64_t cols = (m - j0 < BM) ? m - j0 : BM;
+    OQR_TRY(cudaMemcpy2DAsync(A_dev + j0 * ldda + j0, ldda * sizeof(double), A_host + j0 * lda + j0,
+                              lda * sizeof(double), (m - j0) * sizeof(double), cols, cudaMemcpyHostToDevice, s));
+  }
+  return 0;
+}
+
 int oqr_normal_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
                        double* Q, double* R, oqr_stream_t stream) {
   int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);

@@ -348,3 +348,14 @@ def test_sym_determinism(oqr):
     A, Z = to_dev(p.A), to_dev(p.Z)
     G1, G2 = oqr.gram_sym(A, Z), oqr.gram_sym(A, Z)
     assert torch.equal(G1, G2)
+
+
+def test_upload_sym_copies_what_sym_reads(oqr):
+    p = make(333, 21, 1e3, 1e2, 23)
+    A_h = torch.from_numpy(p.A)                       # (m, lda) column-major host A
+    A_d = torch.full_like(A_h, float("nan"), device=DEV)
+    oqr.upload_sym(A_h, A_d)
+    torch.cuda.synchronize()
+    Q1, R1, s1 = oqr.normal_sym(A_d, to_dev(p.Z))
+    Q2, R2, s2 = oqr.normal_sym(to_dev(p.A), to_dev(p.Z))
+    assert s1 == s2 == 0 and torch.equal(R1, R2) and torch.equal(Q1, Q2)
