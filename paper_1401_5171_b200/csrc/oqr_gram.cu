@@ -17,6 +17,7 @@
 // column halves) keep W_I in DMMA accumulators.
 #include <cuda.h>  // CUtensorMap and its enums (the encode entry point is fetched at run time)
 
+#include <cstdlib>
 #include <cstring>
 
 #include "oqr_internal.cuh"
@@ -183,6 +184,15 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
   static_assert(NCH * LG * 64 == NCW * 32, "one chunk entry per thread");
+#ifdef OQR_EXP_NOCONTRACT  // experiment build only (tools/exp): measures the contraction's share
+  {
+    double t = 0.0;  // consume every accumulator (else ptxas drops the DMMAs)
+#pragma unroll
+    for (int i = 0; i < NTW; ++i) t += acc[i][0] + acc[i][1];
+    slot[ctid] = first ? t : slot[ctid] + t;
+    return;
+  }
+#endif
   // 1. Re-distribute W from accumulator layout to B-operand layout (rows = i, cols = l):
   //    wb[t][h] = W[rg*8 + 4h + lane%4, (ch*NTW + t)*8 + lane/4].
   double wb[NTW][2];
@@ -251,9 +261,11 @@ __host__ __device__ __forceinline__ int unit_nk(int I, int KB) {
   return SYM ? min(KB, (I + 1) * (BM / BK)) : KB;
 }
 // Balanced split of the unit range over the CTAs: a panel costs its units plus one contraction
-// (~PANEL_W units of DMMA time), so the split equalises W(u) = u + PANEL_W * (panels started
-// before u) instead of u alone -- the symmetric schedule has panels of 4 .. KB units.
-constexpr int PANEL_W = 24;
+// (~panel_w units of time), so the split equalises W(u) = u + panel_w * (panels started before
+// u) instead of u alone -- the symmetric schedule has panels of 4 .. KB units.  The contraction
+// is ~NT times costlier than one unit relative to the unit's NT-proportional work, so
+// panel_w = PANEL_W_PER_NT * NT (calibrated on B200: tools/time_k1.py, OQR_PANEL_W overrides).
+constexpr double PANEL_W_PER_NT = 2.0;
 
 template <bool SYM>
 __host__ __device__ __forceinline__ int unit_panels_before(int u, int KB) {  // panels starting at < u
@@ -266,14 +278,14 @@ __host__ __device__ __forceinline__ int unit_panels_before(int u, int KB) {  // 
 }
 
 template <bool SYM>
-__device__ __forceinline__ int unit_split(int c, int g, int U, int KB, int npanels) {
+__device__ __forceinline__ int unit_split(int c, int g, int U, int KB, int npanels, double panel_w) {
   if (c <= 0) return 0;
   if (c >= g) return U;
-  const double target = ((double)U + (double)PANEL_W * npanels) * c / g;
+  const double target = ((double)U + panel_w * npanels) * c / g;
   int lo = 0, hi = U;  // smallest u with W(u) >= target
   while (lo < hi) {
     const int mid = lo + (hi - lo) / 2;
-    if ((double)mid + (double)PANEL_W * unit_panels_before<SYM>(mid, KB) >= target) hi = mid;
+    if ((double)mid + panel_w * unit_panels_before<SYM>(mid, KB) >= target) hi = mid;
     else lo = mid + 1;
   }
   return lo;
@@ -444,7 +456,8 @@ template <int NT, bool SYM>
 __global__ void __launch_bounds__(NCW * 32, 1)
 gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t mr, const double* __restrict__ A,
                   int64_t lda, const double* __restrict__ Zp, const double* __restrict__ Zc,
-                  const double* __restrict__ Zh, double* __restrict__ P, int KB, int U, int stages, bool tma_ok) {
+                  const double* __restrict__ Zh, double* __restrict__ P, int KB, int U, int stages, bool tma_ok,
+                  double panel_w) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
   constexpr int STAGE = BM * BK + NT * 4 * FRAG;  // doubles per pipeline stage
@@ -459,7 +472,8 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
   const int rg = warp % NRG, ch = warp / NRG;
   const int g = gridDim.x, c = blockIdx.x;
   const int npanels = (int)cdiv(mr, BM);
-  const int u0 = unit_split<SYM>(c, g, U, KB, npanels), u1 = unit_split<SYM>(c + 1, g, U, KB, npanels);
+  const int u0 = unit_split<SYM>(c, g, U, KB, npanels, panel_w);
+  const int u1 = unit_split<SYM>(c + 1, g, U, KB, npanels, panel_w);
   if (u0 >= u1) {  // the weighted split can leave a CTA without units: its slot is zero
     double* slot = P + c * (int64_t)NP * NP;
     for (int e = threadIdx.x; e < NP * NP; e += blockDim.x) slot[e] = 0.0;
@@ -740,8 +754,10 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
   std::memset(&tmap, 0, sizeof(tmap));
   const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda);
   timing_begin(s);
+  static const char* env_w = getenv("OQR_PANEL_W");
+  const double panel_w = env_w ? atof(env_w) : PANEL_W_PER_NT * NT;
   gram_fused_kernel<NT, SYM><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, Zh, P, (int)KB,
-                                                                  (int)U, stages, tma_ok);
+                                                                  (int)U, stages, tma_ok, panel_w);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);

@@ -9,6 +9,5 @@ F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -
 build() { /usr/local/cuda/bin/nvcc $F $2 -o tools/exp/liboqr_$1.so $SRC; }
 build NODMMA "-DOQR_EXP_NODMMA" &
 build NOLOAD "-DOQR_EXP_NOLOAD" &
-build NODMMA_NOA "-DOQR_EXP_NODMMA -DOQR_EXP_NOA" &
-build NODMMA_NOZ "-DOQR_EXP_NODMMA -DOQR_EXP_NOZ" &
+build NOCONTRACT "-DOQR_EXP_NOCONTRACT" &
 wait
