@@ -122,6 +122,23 @@ int oqr_normal2_tridiag(int64_t m, int64_t n, const double* d, const double* e, 
 int oqr_prequr_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
                        double* Q, double* R, oqr_stream_t stream);
 
+/*
+ * oqr_prequr_stable -- PRE-CHOLQR (Algorithm 2) with a STABLE Euclidean pre-step
+ * (reading R21): shifted CholeskyQR3 (Fukaya et al., SIAM J. Sci.
+ * Comput. 42, 2020) -- G = Z^T Z, R1 = chol(G + 11 (m n + n(n+1)) u tr(G) I), Q1 = Z R1^{-1}, two
+ * Cholesky-QR passes on Q1 (R2, R3), Y = Q3, S = R3 R2 R1 -- a backward-stable QR of Z for
+ * kappa(Z) up to ~1/u, which is what Theorem 3 assumes of the pre-step; then
+ * [Q, U] = CHOLQR(A, Y) and R = U S.  Removes the kappa(Z) <~ 1e7.5 limit of oqr_prequr.
+ * Breakdown in any pre-step Cholesky: code k; in the A-stage: n + k.  Y lives in Q.
+ * _sym / _tridiag: the same with the symmetric (block-lower) or tridiagonal A-stage.
+ */
+int oqr_prequr_stable(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                      double* Q, double* R, oqr_stream_t stream);
+int oqr_prequr_stable_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                          double* Q, double* R, oqr_stream_t stream);
+int oqr_prequr_stable_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z,
+                              int64_t ldz, double* Q, double* R, oqr_stream_t stream);
+
 /* Human-readable text for a status code (static storage; never NULL). */
 const char* oqr_status_string(int status);
 

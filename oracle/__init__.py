@@ -62,6 +62,8 @@ def _load():
             "orc_dd_chol_resid": (None, [I, P, I, P, I, P, P]),
             "orc_dd_orth_cols": (None, [I, I, P, P, I, P, I, P]),
             "orc_gram_tridiag": (None, [I, I, P, P, P, I, P, I]),
+            "orc_scqr3": (ctypes.c_int, [I, I, P, I, P, P]),
+            "orc_prequr_stable": (ctypes.c_int, [I, I, P, I, P, I, P, P]),
             "orc_normal_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
             "orc_normal2_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
             "orc_prequr_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
@@ -170,7 +172,22 @@ def prequr(A, Z, m):
     return _variant("orc_prequr", A, Z, m)
 
 
-VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr}
+def prequr_stable(A, Z, m):
+    """PRE-CHOLQR with the stable (shifted CholeskyQR3) Euclidean pre-step (NEXT-N1, reading R21)."""
+    return _variant("orc_prequr_stable", A, Z, m)
+
+
+def scqr3(Z, m):
+    """Shifted CholeskyQR3 of Z: (Y storage (n, m), S storage (n, n), info)."""
+    Z, ldz = _cm(Z, m)
+    n = Z.shape[0]
+    Y = np.zeros((n, m))
+    S = np.zeros((n, n))
+    info = _load().orc_scqr3(m, n, _p(Z), ldz, _p(Y), _p(S))
+    return Y, S, info
+
+
+VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr, "prequr_stable": prequr_stable}
 
 
 # -------------------------------------------------------------- checkers ---

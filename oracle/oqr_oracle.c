@@ -468,3 +468,66 @@ void orc_dd_orth_tridiag(int64_t m, int64_t n, const double* d, const double* e,
     }
   free(AQ);
 }
+
+/* ========================================================================= */
+/* NEXT-N1: PRE-CHOLQR with a STABLE Euclidean pre-step (reading R21). */
+/* Theorem 3 assumes a backward-stable Euclidean QR of Z; the */
+/* pre-step here is shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto,  */
+/* Yanagisawa, SIAM J. Sci. Comput. 42 (2020)), stable for kappa(Z) <~ 1/u:       */
+/*   G = Z^T Z;  s = 11 (m n + n (n+1)) u tr(G)   (tr(G) = ||Z||_F^2 >= ||Z||_2^2,  */
+/*   summed i ascending);  R1 = chol(G + s I);  Q1 = Z / R1;                        */
+/*   [Q2, R2] = CholQR(Q1);  [Y, R3] = CholQR(Q2);  S = R3 R2 R1;                   */
+/* then the A-stage [Q, U] = CHOLQR(A, Y) and R = U S.          */
+/* Breakdown in any pre-step Cholesky -> k; in the A-stage -> n + k.              */
+/* ========================================================================= */
+static int orc_cholqr_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* Q, double* R,
+                             double shift_factor) {
+  double* G = (double*)malloc(sizeof(double) * n * n);
+  orc_gram_euclid(m, n, Z, ldz, G, n);
+  if (shift_factor > 0.0) {
+    double tr = 0.0;
+    for (int64_t i = 0; i < n; i++) tr += G[i * n + i];
+    const double s = shift_factor * tr;
+    for (int64_t i = 0; i < n; i++) G[i * n + i] += s;
+  }
+  int info = orc_potrf(n, G, n, R, n);
+  free(G);
+  if (info) return info;
+  orc_trsm(m, n, Z, ldz, R, n, Q, m);
+  return 0;
+}
+
+int orc_scqr3(int64_t m, int64_t n, const double* Z, int64_t ldz, double* Y, double* S) {
+  const double u = 0x1.0p-53;
+  const double shift_factor = 11.0 * ((double)m * (double)n + (double)n * (double)(n + 1)) * u;
+  double* R1 = (double*)malloc(sizeof(double) * n * n);
+  double* R2 = (double*)malloc(sizeof(double) * n * n);
+  double* R3 = (double*)malloc(sizeof(double) * n * n);
+  double* T = (double*)malloc(sizeof(double) * n * n);
+  double* Q1 = (double*)malloc(sizeof(double) * m * n);
+  double* Q2 = (double*)malloc(sizeof(double) * m * n);
+  int info = orc_cholqr_euclid(m, n, Z, ldz, Q1, R1, shift_factor);
+  if (!info) info = orc_cholqr_euclid(m, n, Q1, m, Q2, R2, 0.0);
+  if (!info) info = orc_cholqr_euclid(m, n, Q2, m, Y, R3, 0.0);
+  if (!info) {
+    orc_trmm(n, R3, n, R2, n, T, n);   /* T = R3 R2 */
+    orc_trmm(n, T, n, R1, n, S, n);    /* S = T R1  */
+  }
+  free(R1); free(R2); free(R3); free(T); free(Q1); free(Q2);
+  return info;
+}
+
+int orc_prequr_stable(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                      double* Q, double* R) {
+  double* S = (double*)malloc(sizeof(double) * n * n);
+  double* U = (double*)malloc(sizeof(double) * n * n);
+  double* Y = (double*)malloc(sizeof(double) * m * n);
+  int info = orc_scqr3(m, n, Z, ldz, Y, S);
+  if (!info) {
+    int info2 = orc_normal(m, n, A, lda, Y, m, Q, U);
+    if (info2) info = (int)n + info2;
+    else orc_trmm(n, U, n, S, n, R, n);
+  }
+  free(S); free(U); free(Y);
+  return info;
+}

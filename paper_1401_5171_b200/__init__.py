@@ -24,7 +24,8 @@ __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm"
            "launch_count", "EXPORTS"]
 
 # Every symbol include/oqr.h declares.
-EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
+EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_prequr_stable", "oqr_prequr_stable_sym",
+           "oqr_prequr_stable_tridiag", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
            "oqr_gram_sym", "oqr_upload_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
            "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_gram_rows", "oqr_sum_partials",
@@ -50,11 +51,11 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(LIB_PATH)
         I64, P, I = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
         for name in ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_sym", "oqr_normal2_sym",
-                     "oqr_prequr_sym"):
+                     "oqr_prequr_sym", "oqr_prequr_stable", "oqr_prequr_stable_sym"):
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, I64, P, I64, P, P, P]
-        for name in ("oqr_normal_tridiag", "oqr_normal2_tridiag", "oqr_prequr_tridiag"):
+        for name in ("oqr_normal_tridiag", "oqr_normal2_tridiag", "oqr_prequr_tridiag", "oqr_prequr_stable_tridiag"):
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, P, P, I64, P, P, P]
@@ -149,7 +150,12 @@ def prequr(A, Z, Q=None, R=None, stream=None, check: bool = True):
     return _variant("oqr_prequr", A, Z, Q, R, stream, check)
 
 
-VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr}
+def prequr_stable(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    """PRE-CHOLQR with the stable shifted-CholeskyQR3 Euclidean pre-step (NEXT-N1, reading R21)."""
+    return _variant("oqr_prequr_stable", A, Z, Q, R, stream, check)
+
+
+VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr, "prequr_stable": prequr_stable}
 
 
 def normal_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
@@ -165,7 +171,11 @@ def prequr_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
     return _variant("oqr_prequr_sym", A, Z, Q, R, stream, check)
 
 
-VARIANTS_SYM = {"normal": normal_sym, "normal2": normal2_sym, "prequr": prequr_sym}
+def prequr_stable_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant("oqr_prequr_stable_sym", A, Z, Q, R, stream, check)
+
+
+VARIANTS_SYM = {"normal": normal_sym, "normal2": normal2_sym, "prequr": prequr_sym, "prequr_stable": prequr_stable_sym}
 
 
 def upload_sym(A_host, A_dev, stream=None):
@@ -231,7 +241,12 @@ def prequr_tridiag(d, e, Z, Q=None, R=None, stream=None, check: bool = True):
     return _variant_tridiag("oqr_prequr_tridiag", d, e, Z, Q, R, stream, check)
 
 
-VARIANTS_TRIDIAG = {"normal": normal_tridiag, "normal2": normal2_tridiag, "prequr": prequr_tridiag}
+def prequr_stable_tridiag(d, e, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant_tridiag("oqr_prequr_stable_tridiag", d, e, Z, Q, R, stream, check)
+
+
+VARIANTS_TRIDIAG = {"normal": normal_tridiag, "normal2": normal2_tridiag, "prequr": prequr_tridiag,
+                    "prequr_stable": prequr_stable_tridiag}
 
 
 def gram_tridiag(d, e, Z, G=None, stream=None):

@@ -62,6 +62,8 @@ struct Workspace {
   double* G = nullptr;     // n x n Gram
   double* R1 = nullptr;    // n x n (R1 of normal2 / S of prequr)
   double* R2 = nullptr;    // n x n (R2 of normal2 / U of prequr)
+  double* R3 = nullptr;    // n x n (stable pre-step: R2, R3 of the CholeskyQR2 stage)
+  double* R4 = nullptr;    // n x n (stable pre-step: products)
   int* info = nullptr;
   cudaStream_t s = nullptr;
   int alloc(int64_t m, int n, cudaStream_t st, int64_t mr_local = 0) {
@@ -72,7 +74,7 @@ struct Workspace {
     const size_t zc = mr_local > 0 ? (size_t)zp_doubles(mr_local, NP) : 0;
     const size_t sl = slots_doubles(n, gram_grid(m));
     const size_t nn = (size_t)n * n;
-    const size_t total = zp + zc + sl + 3 * nn + 2;  // +2 doubles (16 B) for info
+    const size_t total = zp + zc + sl + 5 * nn + 2;  // +2 doubles (16 B) for info
     if (cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), st) != cudaSuccess) {
       cudaGetLastError();
       base = nullptr;
@@ -84,7 +86,9 @@ struct Workspace {
     G = P + sl;
     R1 = G + nn;
     R2 = R1 + nn;
-    info = reinterpret_cast<int*>(R2 + nn);
+    R3 = R2 + nn;
+    R4 = R3 + nn;
+    info = reinterpret_cast<int*>(R4 + nn);
     return 0;
   }
   ~Workspace() {
@@ -167,7 +171,7 @@ static int cholqr_pass(const AOp& op, int64_t m, int n, const double* Z, int64_t
                        int info_off, Workspace& ws, cudaStream_t s) {
   int st = gram_into(op, m, n, Z, ldz, ws.G, ws, s);
   if (st) return st;
-  OQR_TRY(launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s));
+  OQR_TRY(launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s, info_off == 0));
   OQR_TRY(launch_trsm(m, n, Z, ldz, Rout, n, Q, m, ws.info, s));
   return 0;
 }
@@ -221,6 +225,33 @@ static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t 
   if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
   // R = U S
   if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R1, R, ws.info, s)))) return st;
+  return finish(ws, s);
+}
+
+// PRE-CHOLQR with the stable Euclidean pre-step (NEXT-N1, reading R21): shifted CholeskyQR3.
+//   G = Z^T Z, G += 11 (m n + n (n+1)) u tr(G) I, R1 = chol(G), Q1 = Z / R1 (into Q);
+//   two CholeskyQR passes on Q in place (R2, R3); S = R3 R2 R1; then [Q, U] = CHOLQR(A, Y); R = U S.
+static int run_prequr_stable(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
+                             cudaStream_t s) {
+  Workspace ws;
+  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
+  if (st) return st;
+  const double factor = 11.0 * ((double)m * (double)n + (double)n * (double)(n + 1)) * 0x1.0p-53;
+  if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
+  if ((st = cuda_status(launch_shift_diag(n, ws.G, n, factor, nullptr, s)))) return st;
+  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true)))) return st;
+  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s)))) return st;
+  double* Rk[2] = {ws.R2, ws.R3};
+  for (int pass = 0; pass < 2; ++pass) {  // CholeskyQR2 on Q1, in place
+    if ((st = gram_euclid_into(m, n, Q, m, ws.G, ws, s))) return st;
+    if ((st = cuda_status(launch_potrf(n, ws.G, n, Rk[pass], n, ws.info, 0, s, false)))) return st;
+    if ((st = cuda_status(launch_trsm(m, n, Q, m, Rk[pass], n, Q, m, ws.info, s)))) return st;
+  }
+  if ((st = cuda_status(launch_trmm(n, ws.R3, ws.R2, ws.R4, ws.info, s)))) return st;  // R3 R2
+  if ((st = cuda_status(launch_trmm(n, ws.R4, ws.R1, ws.R3, ws.info, s)))) return st;  // S = (R3 R2) R1
+  // A-stage: [Q, U] = CHOLQR(A, Y) in place (U into R2); breakdown code n + k
+  if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
+  if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R3, R, ws.info, s)))) return st;   // R = U S
   return finish(ws, s);
 }
 
@@ -278,6 +309,28 @@ int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double*
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
   return run_prequr(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_prequr_stable(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                      double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  return run_prequr_stable(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_prequr_stable_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                          double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  return run_prequr_stable(dense_op(A, lda, true), m, (int)n, Z, ldz, Q, R,
+                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_prequr_stable_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z,
+                              int64_t ldz, double* Q, double* R, oqr_stream_t stream) {
+  int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
+  if (st) return st;
+  return run_prequr_stable(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_normal_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
@@ -433,7 +486,7 @@ int oqr_potrf(int64_t n, const double* G, double* R, int* d_info, oqr_stream_t s
   if (n < 1 || n > OQR_NMAX) return -2;
   if (G == nullptr || R == nullptr || d_info == nullptr) return -3;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  return cuda_status(launch_potrf((int)n, G, n, R, n, d_info, 0, s));
+  return cuda_status(launch_potrf((int)n, G, n, R, n, d_info, 0, s, true));
 }
 
 int oqr_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, double* Q,

@@ -26,10 +26,10 @@ __device__ __forceinline__ void dmma_c(double (&d)[2], double a, double b) {
 
 __global__ void __launch_bounds__(1024, 1)
 potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ R, int64_t ldr,
-             int* info, int info_off) {
+             int* info, int info_off, bool first) {
   extern __shared__ double S[];
   __shared__ int s_brk;
-  if (info_off > 0 && *info != 0) return;  // an earlier stage already broke down
+  if (!first && *info != 0) return;  // an earlier stage already broke down: keep its code
   const int NT = (n + 7) / 8, NP = NT * 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   for (int l = warp; l < NP; l += nwarp)
@@ -101,11 +101,11 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
   }
   for (int l = warp; l < n; l += nwarp)
     for (int k = lane; k < n; k += 32) R[(int64_t)l * ldr + k] = (k <= l) ? S[pk(k, l)] : 0.0;
-  if (tid == 0 && info_off == 0) *info = 0;
+  if (tid == 0 && first) *info = 0;
 }
 
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
-                         int info_off, cudaStream_t s) {
+                         int info_off, cudaStream_t s, bool first) {
   const int NP = 8 * ((n + 7) / 8);
   const size_t bytes = (size_t)NP * (NP + 1) / 2 * sizeof(double);
   static bool attr_done = false;
@@ -115,7 +115,28 @@ cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off);
+  potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off, first);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ shift -----------------
+// G += s I with s = factor * tr(G), tr summed in ascending order (shifted CholeskyQR, reading
+// R21: factor = 11 (m n + n (n + 1)) u, tr(G) = ||Z||_F^2 bounds ||Z||_2^2 from above).
+__global__ void shift_diag_kernel(int n, double* G, int64_t ldg, double factor, const int* info) {
+  __shared__ double s_shift;
+  if (info != nullptr && *info != 0) return;
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += G[(int64_t)i * ldg + i];
+    s_shift = factor * tr;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) G[(int64_t)i * ldg + i] += s_shift;
+}
+
+cudaError_t launch_shift_diag(int n, double* G, int64_t ldg, double factor, const int* info, cudaStream_t s) {
+  shift_diag_kernel<<<1, 256, 0, s>>>(n, G, ldg, factor, info);
   note_launch();
   return cudaGetLastError();
 }

@@ -64,9 +64,12 @@ cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double*
 // G (n x n, ldg) = sum_{c<g} P[c] in fixed c order.
 cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s,
                                bool sym = false);
-// R = chol(G) (upper); *info = 0 | k (info_off == 0), or (only if *info == 0) n + k.
+// R = chol(G) (upper).  first: *info = 0 on success, info_off + k on breakdown.  !first: does
+// nothing if *info != 0 already (an earlier stage broke down), else writes info_off + k on breakdown.
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
-                         int info_off, cudaStream_t s);
+                         int info_off, cudaStream_t s, bool first = true);
+// G += factor * tr(G) * I (skipped when *info != 0).
+cudaError_t launch_shift_diag(int n, double* G, int64_t ldg, double factor, const int* info, cudaStream_t s);
 // Q = Z R^{-1}; skipped when info != nullptr && *info != 0.
 cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
                         double* Q, int64_t ldq, const int* info, cudaStream_t s);

@@ -184,6 +184,9 @@ def _certain_success(A, Zc, m, n, euclid=False):
 
 def outcome_determined(p, variant):
     m, n = p.m, p.n
+    if variant == "prequr_stable":   # stable pre-step: only the A-stage can break down
+        Y, _, info = oracle.scqr3(p.Z, m)
+        return info == 0 and _certain_success(p.A, Y, m, n)
     if variant in ("normal", "normal2"):
         ok = _certain_success(p.A, p.Z, m, n)
         if ok and variant == "normal2":
@@ -235,7 +238,7 @@ def variant_gates(oqr, p, variant, family="dense"):
     return Qg, Rg, st
 
 
-@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_stable"])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
 def test_t2_t5_t6_t7_variants(oqr, shape, variant):
     variant_gates(oqr, make(*shape), variant)
@@ -359,3 +362,49 @@ def test_upload_sym_copies_what_sym_reads(oqr):
     Q1, R1, s1 = oqr.normal_sym(A_d, to_dev(p.Z))
     Q2, R2, s2 = oqr.normal_sym(to_dev(p.A), to_dev(p.Z))
     assert s1 == s2 == 0 and torch.equal(R1, R2) and torch.equal(Q1, Q2)
+
+
+# ---------------------------------------------------- NEXT-N1: stable pre-step (shifted CholeskyQR3)
+@pytest.mark.parametrize("kz", [1e8, 1e10, 1e12])
+def test_prequr_stable_ill_conditioned_Z(oqr, kz):
+    """kappa(Z) beyond the Euclidean Cholesky-QR pre-step's limit (reading R2): oqr_prequr breaks
+    down in its pre-step (kappa >= 1e10), oqr_prequr_stable succeeds with Theorem 3's orthogonality
+    and matches the oracle (gates T2, T5, T6, T7)."""
+    p = gen.problem(2000, 40, 1e6, kz, 61)
+    if kz >= 1e10:
+        _, _, st = oqr.prequr(to_dev(p.A), to_dev(p.Z))
+        assert 1 <= st <= p.n
+    r = variant_gates(oqr, p, "prequr_stable")
+    assert r is not None
+    Qg = r[0]
+    E = oracle.orth_error(p.A, Qg, p.m)
+    scale = U * float(np.max(p.d)) * np.linalg.norm(oracle.from_cm(Qg, p.m), 2) ** 2
+    assert E <= 10 * p.n * scale
+
+
+def test_prequr_stable_beyond_its_range_breaks_down_like_the_oracle(oqr):
+    # shifted CholeskyQR3 is stable for kappa(Z) <~ 1/(11 (m n + n(n+1)) u) (~1e10..1e12 here);
+    # at 1e14 kappa(Q1) ~ 1e9 > u^{-1/2} and the CholeskyQR2 stage breaks down on both sides
+    p = gen.problem(2000, 40, 1e6, 1e14, 61)
+    _, _, st = oqr.prequr_stable(to_dev(p.A), to_dev(p.Z))
+    _, _, sto = oracle.prequr_stable(p.A, p.Z, p.m)
+    assert 1 <= st <= p.n and 1 <= sto <= p.n
+
+
+@pytest.mark.parametrize("family", ["sym", "tridiag"])
+def test_prequr_stable_families(oqr, family):
+    if family == "sym":
+        p = gen.problem(1000, 30, 1e4, 1e11, 62)
+        Q, R, st = oqr.prequr_stable_sym(to_dev(p.A), to_dev(p.Z))
+        Qo, Ro, sto = oracle.prequr_stable(p.A, p.Z, p.m)
+        A_orth = lambda Q: oracle.orth_error(p.A, Q, p.m)
+    else:
+        d, e = gen.tridiag(3000, 1e4)
+        p = gen.problem(3000, 30, 1e4, 1e11, 63, with_A=False)
+        Q, R, st = oqr.prequr_stable_tridiag(torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda(), to_dev(p.Z))
+        Qo, Ro, sto = oracle.prequr_stable(oracle.densify_tridiag(d, e), p.Z, p.m)
+        A_orth = lambda Q: oracle.orth_error_tridiag(d, e, Q, p.m)
+    assert st == 0 and sto == 0
+    Qg, Rg = host(Q), host(R)
+    assert A_orth(Qg) <= 10 * A_orth(Qo) + 1e-12
+    assert oracle.componentwise_ratio(p.Z, Qg, Rg, p.m) <= 10 * oracle.componentwise_ratio(p.Z, Qo, Ro, p.m) + 4 * gamma(p.n + 1)
