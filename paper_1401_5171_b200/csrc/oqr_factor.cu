@@ -10,9 +10,10 @@ namespace oqr {
 // multiple of 8 with an identity block (n = 240 -> 231,360 B).  Blocked right-looking with 8x8
 // blocks -- the same operations as the unblocked algorithm in a different order:
 //   1. warp 0 factors the diagonal block: pivot d = a_pp, breakdown iff !(d > 0) (LAPACK rule,
-//      catches NaN; reading R4), r_pp = sqrt(d), row p of the block divided by r_pp,
-//      the block's trailing triangle updated;
-//   2. one thread per column l solves the block row: r_pl = (a_pl - sum_{c'<c} r_c'p r_c'l)/r_pp;
+//      catches NaN; reading R4), r_pp = sqrt(d), row p of the block scaled by 1/r_pp
+//      (as LAPACK dpotf2), the block's trailing triangle updated;
+//   2. one thread per column l solves the block row: r_pl = (a_pl - sum_{c'<c} r_c'p r_c'l)/r_pp
+//      (multiplying by the block's reciprocals);
 //   3. the trailing upper triangle is updated tile by tile on the FP64 tensor pipe:
 //      A_kl -= R_{j,k}^T R_{j,l} (8x8x8 per tile, mma.m8n8k4 x 2).
 // Only the upper triangle of G is read.
@@ -37,63 +38,90 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
       S[pk(k, l)] = (l < n) ? G[(int64_t)l * ldg + k] : (k == l ? 1.0 : 0.0);
   if (tid == 0) s_brk = 0;
   __syncthreads();
+  __shared__ double s_inv[2][8];  // reciprocals of the diagonal blocks' pivots (double-buffered)
+  // warp 0: factor diagonal block jb (rows/cols jb*8..+8) in place; row p scaled by 1/r_pp as
+  // LAPACK dpotf2 (DSCAL by ONE/AJJ); breakdown (LAPACK rule) recorded in s_brk.
+  auto factor_diag = [&](int jb) {
+    const int b0 = jb * 8;
+    double* inv_out = s_inv[jb & 1];
+    for (int c = 0; c < 8; ++c) {
+      const int p = b0 + c;
+      const double d = S[pk(p, p)];
+      if (!(d > 0.0)) {  // uniform across the warp
+        if (lane == 0) s_brk = p + 1;
+        break;
+      }
+      const double r = sqrt(d);
+      const double inv = 1.0 / r;
+      __syncwarp();
+      if (lane < 7 - c) S[pk(p, p + 1 + lane)] *= inv;
+      if (lane == 0) {
+        S[pk(p, p)] = r;
+        inv_out[c] = inv;
+      }
+      __syncwarp();
+      for (int e = lane; e < 64; e += 32) {
+        const int a = e >> 3, b = e & 7;
+        if (a > c && b >= a) S[pk(b0 + a, b0 + b)] -= S[pk(p, b0 + a)] * S[pk(p, b0 + b)];
+      }
+      __syncwarp();
+    }
+  };
+  // one 8x8 tile of the trailing update: A_{k0.., l0..} -= R_{j0.., k0..}^T R_{j0.., l0..}
+  auto update_tile = [&](int j0, int k0, int l0) {
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int p = j0 + 4 * h + (lane & 3);
+      dmma_c(acc, S[pk(p, k0 + (lane >> 2))], S[pk(p, l0 + (lane >> 2))]);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = k0 + (lane >> 2), l = l0 + 2 * (lane & 3) + e;
+      if (k <= l) S[pk(k, l)] -= acc[e];
+    }
+  };
+  if (warp == 0) factor_diag(0);
   for (int j = 0; j < NT; ++j) {
     const int j0 = j * 8;
-    // 1. diagonal block (warp 0)
-    if (warp == 0) {
-      for (int c = 0; c < 8; ++c) {
-        const int p = j0 + c;
-        const double d = S[pk(p, p)];
-        if (!(d > 0.0)) {  // uniform across the warp
-          if (lane == 0) s_brk = p + 1;
-          break;
-        }
-        const double r = sqrt(d);
-        __syncwarp();
-        if (lane < 7 - c) S[pk(p, p + 1 + lane)] = S[pk(p, p + 1 + lane)] / r;
-        __syncwarp();
-        if (lane == 0) S[pk(p, p)] = r;
-        for (int e = lane; e < 64; e += 32) {
-          const int a = e >> 3, b = e & 7;
-          if (a > c && b >= a) S[pk(j0 + a, j0 + b)] -= S[pk(p, j0 + a)] * S[pk(p, j0 + b)];
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
+    __syncthreads();  // diagonal block j factored (look-ahead by warp 0)
     if (s_brk) break;
+    const double* inv = s_inv[j & 1];
     // 2. block row j: columns l >= j0 + 8 (one thread each), forward substitution with R_jj^T
     for (int l = j0 + 8 + tid; l < NP; l += blockDim.x) {
+      double x[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) x[c] = S[pk(j0 + c, l)];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const int p = j0 + c;
-        double x = S[pk(p, l)];
-        for (int c2 = 0; c2 < c; ++c2) x -= S[pk(j0 + c2, p)] * S[pk(j0 + c2, l)];
-        S[pk(p, l)] = x / S[pk(p, p)];
+        x[c] *= inv[c];
+#pragma unroll
+        for (int c2 = c + 1; c2 < 8; ++c2) x[c2] -= S[pk(j0 + c, j0 + c2)] * x[c];
       }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) S[pk(j0 + c, l)] = x[c];
     }
     __syncthreads();
-    // 3. trailing update on DMMA: tiles (kt, lt), j < kt <= lt < NT
+    // 3. trailing update on DMMA, tiles (kt, lt), j < kt <= lt < NT.  Look-ahead: warp 0 updates
+    //    the next diagonal tile (t = 0) and factors it at once; warps 1.. take the other tiles.
     const int rem = NT - j - 1;
     const int ntiles = rem * (rem + 1) / 2;
-    for (int t = warp; t < ntiles; t += nwarp) {
-      int lt = 0;                                  // t = lt*(lt+1)/2 + kt  (local indices)
-      while ((lt + 1) * (lt + 2) / 2 <= t) ++lt;
-      const int kt = t - lt * (lt + 1) / 2;
-      const int k0 = (j + 1 + kt) * 8, l0 = (j + 1 + lt) * 8;
-      double acc[2] = {0.0, 0.0};
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = j0 + 4 * h + (lane & 3);
-        dmma_c(acc, S[pk(p, k0 + (lane >> 2))], S[pk(p, l0 + (lane >> 2))]);
+    if (warp == 0) {
+      if (rem > 0) {
+        update_tile(j0, j0 + 8, j0 + 8);
+        __syncwarp();
+        factor_diag(j + 1);
       }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int k = k0 + (lane >> 2), l = l0 + 2 * (lane & 3) + e;
-        if (k <= l) S[pk(k, l)] -= acc[e];
+    } else {
+      for (int t = warp; t < ntiles; t += nwarp - 1) {
+        // t = lt*(lt+1)/2 + kt (local indices): closed form with a one-step fix-up
+        int lt = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        if ((lt + 1) * (lt + 2) / 2 <= t) ++lt;
+        if (lt * (lt + 1) / 2 > t) --lt;
+        const int kt = t - lt * (lt + 1) / 2;
+        update_tile(j0, (j + 1 + kt) * 8, (j + 1 + lt) * 8);
       }
     }
-    __syncthreads();
   }
   if (s_brk) {
     if (tid == 0) *info = info_off + s_brk;
