@@ -64,7 +64,13 @@ def normal_rows(Ar, Z, r0: int, mr: int, group=None, steps=None):
     G_r = steps.gram_rows(Ar, Z, r0, mr)
     if world > 1:
         gathered = torch.empty((world, n, n), dtype=G_r.dtype, device=G_r.device)
-        dist.all_gather(list(gathered.unbind(0)), G_r.contiguous(), group=group)  # rank order
+        if G_r.is_cuda and dist.get_backend(group) == "gloo":
+            # gloo exchanges host tensors: stage the 8 n^2-byte partials through host memory
+            host = torch.empty((world, n, n), dtype=G_r.dtype)
+            dist.all_gather(list(host.unbind(0)), G_r.cpu(), group=group)
+            gathered.copy_(host)
+        else:
+            dist.all_gather(list(gathered.unbind(0)), G_r.contiguous(), group=group)  # rank order
     else:
         gathered = G_r.reshape(1, n, n)
     G = steps.sum_partials(gathered)
