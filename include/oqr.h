@@ -23,8 +23,8 @@
  *    upper triangular with positive diagonal; its strictly lower part is written as zero.
  *  - Outputs must not overlap the inputs or each other.
  *  - All work is enqueued on `stream` (0 = legacy default stream).  Scratch memory is
- *    stream-ordered (cudaMallocAsync / cudaFreeAsync) inside the call, so concurrent calls
- *    on different streams are safe.
+ *    stream-ordered (cudaMallocFromPoolAsync / cudaFreeAsync on a memory pool the library owns;
+ *    the device's default pool is not touched), so concurrent calls on different streams are safe.
  *
  * Status codes (LAPACK conventions):
  *     0        success

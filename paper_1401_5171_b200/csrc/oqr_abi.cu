@@ -38,19 +38,27 @@ void timing_end(cudaStream_t s) {
   ++g_event_used;
 }
 
-// One pool setting per process: keep freed stream-ordered blocks cached so that the per-call
-// cudaMallocAsync/cudaFreeAsync pair costs no driver allocation after the first call.
-static void pool_keep_memory() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
+// The library's own stream-ordered memory pool per device (never the device's default pool, whose
+// settings belong to the caller): freed blocks stay cached, so the per-call
+// cudaMallocFromPoolAsync / cudaFreeAsync pair costs no driver allocation after the first call.
+static cudaMemPool_t library_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[dev] = pool;
+  }
+  return pools[dev];
 }
 
 // Stream-ordered scratch for one call.
@@ -67,7 +75,6 @@ struct Workspace {
   int* info = nullptr;
   cudaStream_t s = nullptr;
   int alloc(int64_t m, int n, cudaStream_t st, int64_t mr_local = 0) {
-    pool_keep_memory();
     s = st;
     const int NP = 8 * (int)cdiv(n, 8);
     const size_t zp = (size_t)zp_doubles(m, NP);
@@ -75,7 +82,9 @@ struct Workspace {
     const size_t sl = slots_doubles(n, gram_grid(m));
     const size_t nn = (size_t)n * n;
     const size_t total = zp + zc + sl + 5 * nn + 2;  // +2 doubles (16 B) for info
-    if (cudaMallocAsync(reinterpret_cast<void**>(&base), total * sizeof(double), st) != cudaSuccess) {
+    cudaMemPool_t pool = library_pool();
+    if (pool == nullptr ||
+        cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), total * sizeof(double), pool, st) != cudaSuccess) {
       cudaGetLastError();
       base = nullptr;
       return -101;

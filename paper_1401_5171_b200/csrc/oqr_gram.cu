@@ -256,9 +256,14 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
 // has the k-blocks of the block-lower triangle including its own 64 x 64 diagonal panel,
 // nk(I) = min(KB, 4 (I + 1)), so the units before panel I number 2 I (I + 1) (only the last
 // panel can be clipped).
-template <bool SYM>
+// Stage width: 32 columns of A per stage when n <= 128 (NT <= 16: more DMMA work per stage to
+// amortise the per-stage hand-off), 16 otherwise (the 64 x 16 A tile + NT KiB of Z already fill
+// the ring).  The packed Z layout keeps 16-row blocks (BK); a 32-wide stage moves two of them.
+__host__ __device__ constexpr int stage_k(int NT) { return NT <= 16 ? 32 : 16; }
+
+template <bool SYM, int KS>
 __host__ __device__ __forceinline__ int unit_nk(int I, int KB) {
-  return SYM ? min(KB, (I + 1) * (BM / BK)) : KB;
+  return SYM ? min(KB, (I + 1) * (BM / KS)) : KB;
 }
 // Balanced split of the unit range over the CTAs: a panel costs its units plus one contraction
 // (~panel_w units of time), so the split equalises W(u) = u + panel_w * (panels started before
@@ -267,17 +272,19 @@ __host__ __device__ __forceinline__ int unit_nk(int I, int KB) {
 // panel_w = PANEL_W_PER_NT * NT (calibrated on B200: tools/time_k1.py, OQR_PANEL_W overrides).
 constexpr double PANEL_W_PER_NT = 2.0;
 
-template <bool SYM>
+// SYM: panel I has R (I + 1) units (R = BM / KS), so the units before panel I number R I (I+1)/2.
+template <bool SYM, int KS>
 __host__ __device__ __forceinline__ int unit_panels_before(int u, int KB) {  // panels starting at < u
   if (u <= 0) return 0;
   if (!SYM) return (u + KB - 1) / KB;
-  int i = (int)((sqrt(2.0 * (double)u + 1.0) - 1.0) * 0.5);
-  while (2LL * (i + 1) * (i + 2) < (long long)u) ++i;     // largest i with start(i) = 2i(i+1) < u
-  while (i > 0 && 2LL * i * (i + 1) >= (long long)u) --i;
+  constexpr long long R = BM / KS;
+  int i = (int)((sqrt(8.0 * (double)u / (double)R + 1.0) - 1.0) * 0.5);
+  while (R * (i + 1) * (i + 2) / 2 < (long long)u) ++i;     // largest i with start(i) < u
+  while (i > 0 && R * i * (i + 1) / 2 >= (long long)u) --i;
   return i + 1;
 }
 
-template <bool SYM>
+template <bool SYM, int KS>
 __device__ __forceinline__ int unit_split(int c, int g, int U, int KB, int npanels, double panel_w) {
   if (c <= 0) return 0;
   if (c >= g) return U;
@@ -285,43 +292,45 @@ __device__ __forceinline__ int unit_split(int c, int g, int U, int KB, int npane
   int lo = 0, hi = U;  // smallest u with W(u) >= target
   while (lo < hi) {
     const int mid = lo + (hi - lo) / 2;
-    if ((double)mid + panel_w * unit_panels_before<SYM>(mid, KB) >= target) hi = mid;
+    if ((double)mid + panel_w * unit_panels_before<SYM, KS>(mid, KB) >= target) hi = mid;
     else lo = mid + 1;
   }
   return lo;
 }
 
-template <bool SYM>
+template <bool SYM, int KS>
 __host__ __device__ __forceinline__ void unit_locate(int u, int KB, int* I, int* kb) {
   if (!SYM) {
     *I = u / KB;
     *kb = u - *I * KB;
     return;
   }
-  int i = (int)((sqrt(2.0 * (double)u + 1.0) - 1.0) * 0.5);
-  while (2LL * (i + 1) * (i + 2) <= (long long)u) ++i;
-  while (i > 0 && 2LL * i * (i + 1) > (long long)u) --i;
+  constexpr long long R = BM / KS;
+  int i = (int)((sqrt(8.0 * (double)u / (double)R + 1.0) - 1.0) * 0.5);
+  while (R * (i + 1) * (i + 2) / 2 <= (long long)u) ++i;
+  while (i > 0 && R * i * (i + 1) / 2 > (long long)u) --i;
   *I = i;
-  *kb = u - 2 * i * (i + 1);
+  *kb = (int)(u - R * i * (i + 1) / 2);
 }
 
-// Fill a ring slot with unit (panel I, k-block kb): the A tile A[I*BM.., kb*BK..] (64 x 16,
-// column-major in smem, 8 KiB) and the packed Z block kb (NT KiB).  Executed by warp 0's lanes.
+// Fill a ring slot with unit (panel I, k-block kb): the A tile A[I*BM.., kb*KS..] (64 x KS,
+// column-major in smem) and the KS/16 packed Z blocks of the k-block (NT KiB each).  Executed by warp 0's lanes.
 // With a tensor map (A 16-byte aligned, lda even) both are single async requests and ragged
 // tiles need nothing special: TMA zero-fills rows/columns >= m.  Otherwise the A tile is loaded
 // with plain loads and zero fill (correct, slow).
-template <int NT, bool SYM>
+template <int NT, bool SYM, int KS>
 __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr, const CUtensorMap* tmap,
                                             const double* __restrict__ A, int64_t lda,
                                             const double* __restrict__ Zp, const double* __restrict__ Zh,
                                             double* As, uint64_t* bar, int lane, uint64_t pol_a, uint64_t pol_z,
                                             bool tma_ok) {
-  constexpr uint32_t zbytes = NT * 4 * FRAG * 8;
-  constexpr uint32_t abytes = BM * BK * 8;
-  const int64_t row0 = (int64_t)I * BM, col0 = (int64_t)kb * BK;
-  double* Zs = As + BM * BK;
-  // SYM: the diagonal panel's k-blocks (kb >= 4 I) use Z / 2 (exact), so T = S + D/2 and G = T + T^T
-  const double* zsrc = ((SYM && kb >= I * (BM / BK)) ? Zh : Zp) + kb * (int64_t)(NT * 4 * FRAG);
+  constexpr int ZB = KS / BK;                     // packed Z blocks per stage
+  constexpr uint32_t zbytes = ZB * NT * 4 * FRAG * 8;
+  constexpr uint32_t abytes = BM * KS * 8;
+  const int64_t row0 = (int64_t)I * BM, col0 = (int64_t)kb * KS;
+  double* Zs = As + BM * KS;
+  // SYM: the diagonal panel's k-blocks (kb >= I BM/KS) use Z / 2 (exact): T = S + D/2, G = T + T^T
+  const double* zsrc = ((SYM && kb >= I * (BM / KS)) ? Zh : Zp) + kb * (int64_t)(ZB * NT * 4 * FRAG);
 #ifdef OQR_EXP_NOLOAD  // experiment build only (tools/exp): no copies, barrier still completes
   if (lane == 0) mbar_arrive(bar);
   __syncwarp();
@@ -334,7 +343,7 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr
       bulk_g2s(Zs, zsrc, zbytes, bar, pol_z);
     }
   } else {
-    for (int e = lane; e < BK * BM; e += 32) {
+    for (int e = lane; e < KS * BM; e += 32) {
       const int k = e / BM, r = e - k * BM;
       double v = 0.0;
       if (row0 + r < mr && col0 + k < m) v = A[(col0 + k) * lda + row0 + r];
@@ -354,7 +363,7 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr
 // NTW for the first column half, NT - NTW for the second (one less when NT is odd), so no
 // DMMA is predicated.  Unit bookkeeping is incremental int32 (no division in the loop):
 // (I, kb) is the unit being consumed, (Ii, kbi) the unit `stages` ahead that a refill loads.
-template <int NT, int NTL, bool SYM>
+template <int NT, int NTL, bool SYM, int KS>
 __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m, int64_t mr,
                                               const double* __restrict__ A, int64_t lda,
                                               const double* __restrict__ Zp, const double* __restrict__ Zc,
@@ -364,7 +373,8 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
                                               bool tma_ok, int rg, int ch, int lane, uint64_t pol_a,
                                               uint64_t pol_z) {
   constexpr int NTW = (NT + 1) / 2;
-  constexpr int STAGE = BM * BK + NT * 4 * FRAG;
+  constexpr int ZB = KS / BK;
+  constexpr int STAGE = BM * KS + ZB * NT * 4 * FRAG;
   static_assert(NTL <= NTW, "tile split");
   double acc[NTW][2];
 #pragma unroll
@@ -373,16 +383,16 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
   int s = 0;
   uint32_t ph = 0;
   int I, kb;
-  unit_locate<SYM>(u0, KB, &I, &kb);
-  int nk = unit_nk<SYM>(I, KB);
+  unit_locate<SYM, KS>(u0, KB, &I, &kb);
+  int nk = unit_nk<SYM, KS>(I, KB);
   int ui = u0 + stages;  // next unit to be loaded into the slot being released
   int Ii, kbi;
-  unit_locate<SYM>(ui, KB, &Ii, &kbi);
-  int nki = unit_nk<SYM>(Ii, KB);
+  unit_locate<SYM, KS>(ui, KB, &Ii, &kbi);
+  int nki = unit_nk<SYM, KS>(Ii, KB);
   // A fragment: A[row0 + rg*8 + lane/4, col0 + kk*4 + lane%4] from the column-major 64 x 16 tile
   const int a_off = (lane & 3) * BM + rg * 8 + (lane >> 2);
-  // B fragment (lt, kk): 32 consecutive doubles of the packed block
-  const int b_off = BM * BK + ch * NTW * 4 * FRAG + lane;
+  // B fragment (block zb, lt, kk): 32 consecutive doubles of the packed blocks
+  const int b_off = BM * KS + ch * NTW * 4 * FRAG + lane;
   for (int u = u0; u < u1; ++u) {
     mbar_wait(&full[s], ph);
     const double* As = ring + s * STAGE;
@@ -392,16 +402,17 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
 #pragma unroll
     for (int t = 0; t < NTL; ++t) b_cur[t] = Zs[t * 4 * FRAG];
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
+    for (int kk = 0; kk < KS / 4; ++kk) {
       double a_nxt = 0.0, b_nxt[NTL > 0 ? NTL : 1];
-      if (kk + 1 < BK / 4) {
-        a_nxt = As[(kk + 1) * 4 * BM + a_off];
+      if (kk + 1 < KS / 4) {
+        const int k1 = kk + 1, zb = k1 >> 2, k4 = k1 & 3;
+        a_nxt = As[k1 * 4 * BM + a_off];
 #pragma unroll
-        for (int t = 0; t < NTL; ++t) b_nxt[t] = Zs[(t * 4 + kk + 1) * FRAG];
+        for (int t = 0; t < NTL; ++t) b_nxt[t] = Zs[((zb * NT + t) * 4 + k4) * FRAG];
       }
 #pragma unroll
       for (int t = 0; t < NTL; ++t) dmma(acc[t], a_cur, b_cur[t]);
-      if (kk + 1 < BK / 4) {
+      if (kk + 1 < KS / 4) {
         a_cur = a_nxt;
 #pragma unroll
         for (int t = 0; t < NTL; ++t) b_cur[t] = b_nxt[t];
@@ -419,14 +430,14 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last && ui < u1) {
       mbar_wait(&empty[s], ph);
-      issue_stage<NT, SYM>(Ii, kbi, m, mr, tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
-                           tma_ok);
+      issue_stage<NT, SYM, KS>(Ii, kbi, m, mr, tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a,
+                               pol_z, tma_ok);
     }
     ++ui;
     if (++kbi == nki) {
       kbi = 0;
       ++Ii;
-      nki = unit_nk<SYM>(Ii, KB);
+      nki = unit_nk<SYM, KS>(Ii, KB);
     }
     if (++s == stages) {
       s = 0;
@@ -442,7 +453,7 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     if (panel_end) {
       kb = 0;
       ++I;
-      nk = unit_nk<SYM>(I, KB);
+      nk = unit_nk<SYM, KS>(I, KB);
     }
   }
 }
@@ -460,7 +471,8 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
                   double panel_w) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
-  constexpr int STAGE = BM * BK + NT * 4 * FRAG;  // doubles per pipeline stage
+  constexpr int KS = stage_k(NT);
+  constexpr int STAGE = BM * KS + (KS / BK) * NT * 4 * FRAG;  // doubles per pipeline stage
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
@@ -472,8 +484,8 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
   const int rg = warp % NRG, ch = warp / NRG;
   const int g = gridDim.x, c = blockIdx.x;
   const int npanels = (int)cdiv(mr, BM);
-  const int u0 = unit_split<SYM>(c, g, U, KB, npanels, panel_w);
-  const int u1 = unit_split<SYM>(c + 1, g, U, KB, npanels, panel_w);
+  const int u0 = unit_split<SYM, KS>(c, g, U, KB, npanels, panel_w);
+  const int u1 = unit_split<SYM, KS>(c + 1, g, U, KB, npanels, panel_w);
   if (u0 >= u1) {  // the weighted split can leave a CTA without units: its slot is zero
     double* slot = P + c * (int64_t)NP * NP;
     for (int e = threadIdx.x; e < NP * NP; e += blockDim.x) slot[e] = 0.0;
@@ -496,17 +508,17 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
   if (warp == 0) {
     for (int s = 0; s < stages && u0 + s < u1; ++s) {
       int I, kb;
-      unit_locate<SYM>(u0 + s, KB, &I, &kb);
-      issue_stage<NT, SYM>(I, kb, m, mr, &tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
-                           tma_ok);
+      unit_locate<SYM, KS>(u0 + s, KB, &I, &kb);
+      issue_stage<NT, SYM, KS>(I, kb, m, mr, &tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
+                               tma_ok);
     }
   }
   double* slot = P + c * (int64_t)NP * NP;
   if (ch == 0)
-    consume_units<NT, NTW, SYM>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB, u0,
+    consume_units<NT, NTW, SYM, KS>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB, u0,
                                 u1, stages, tma_ok, rg, ch, lane, pol_a, pol_z);
   else
-    consume_units<NT, NT - NTW, SYM>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB,
+    consume_units<NT, NT - NTW, SYM, KS>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB,
                                      u0, u1, stages, tma_ok, rg, ch, lane, pol_a, pol_z);
 }
 
@@ -690,7 +702,8 @@ size_t slots_doubles(int n, int g) {
 }
 
 static int fused_stages(int NT, size_t* bytes) {
-  const size_t stage = (size_t)(BM * BK + NT * 4 * FRAG) * 8;
+  const int KS = stage_k(NT);
+  const size_t stage = (size_t)(BM * KS + (KS / BK) * NT * 4 * FRAG) * 8;
   const size_t fixed = 256 + (size_t)NCH * NRG * LG * 64 * 8;
   int st = (int)((SMEM_MAX - fixed) / stage);
   if (st > 8) st = 8;
@@ -716,15 +729,15 @@ static EncodeTiledFn encode_fn() {
 }
 
 // A (or a row block of it) as a 2-D FP64 tensor {rows mr (contiguous), cols m (stride lda)},
-// box {BM, BK}, no swizzle,
+// box {BM, KS}, no swizzle,
 // out-of-bounds elements zero-filled.
-static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t mr, int64_t m, int64_t lda) {
+static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t mr, int64_t m, int64_t lda, int ks) {
   if ((reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0 || m > (int64_t)INT32_MAX) return false;
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)mr, (cuuint64_t)m};
   const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)BK};
+  const cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)ks};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -743,19 +756,22 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int64_t KB = cdiv(m, BK), NPAN = cdiv(mr, BM);
-  // U < 2^31 for every m that fits in HBM.  SYM: 2 P (P - 1) units before the last panel.
-  const int64_t U = SYM ? 2 * (NPAN - 1) * NPAN + unit_nk<true>((int)(NPAN - 1), (int)KB) : NPAN * KB;
+  constexpr int KS = stage_k(NT);
+  const int64_t KB = cdiv(m, KS), NPAN = cdiv(mr, BM);
+  // U < 2^31 for every m that fits in HBM.  SYM: R P (P - 1)/2 units before the last panel.
+  const int64_t R = BM / KS;
+  const int64_t U = SYM ? R * (NPAN - 1) * NPAN / 2 + unit_nk<true, KS>((int)(NPAN - 1), (int)KB) : NPAN * KB;
   if (U > (int64_t)INT32_MAX - 64) return cudaErrorInvalidValue;
   int64_t g = num_sms();
   if (g > U) g = U;
   *g_out = (int)g;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda);
+  const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda, KS);
   timing_begin(s);
   static const char* env_w = getenv("OQR_PANEL_W");
-  const double panel_w = env_w ? atof(env_w) : PANEL_W_PER_NT * NT;
+  // panel weight in units: a unit carries KS/16 times the work of a 16-wide unit
+  const double panel_w = env_w ? atof(env_w) : PANEL_W_PER_NT * NT * (16.0 / KS);
   gram_fused_kernel<NT, SYM><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, Zh, P, (int)KB,
                                                                   (int)U, stages, tma_ok, panel_w);
   note_launch();
