@@ -66,12 +66,17 @@ def sampled_cols(n):
     return sorted(set([0, 1, 2, 3, n // 2, n - 3, n - 2, n - 1]))[:SAMPLE_COLS]
 
 
-@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_stable", "normal_sym", "prequr_sym"])
 def test_variants_full(case, variant):
     p, oqr = case["p"], case["oqr"]
     m, n = p.m, p.n
-    Q, R, st = oqr.VARIANTS[variant](case["A"], case["Z"])
-    Q2, R2, st2 = oqr.VARIANTS[variant](case["A"], case["Z"])
+    if variant.endswith("_sym"):      # NEXT-N4: same mathematics, block-lower triangle of A only
+        variant = variant[:-4]
+        fn = oqr.VARIANTS_SYM[variant]
+    else:
+        fn = oqr.VARIANTS[variant]
+    Q, R, st = fn(case["A"], case["Z"])
+    Q2, R2, st2 = fn(case["A"], case["Z"])
     assert st == st2                                                            # T8
     if st == 0:                        # on breakdown Q and R are unspecified (include/oqr.h)
         assert torch.equal(Q, Q2) and torch.equal(R, R2)
@@ -80,7 +85,7 @@ def test_variants_full(case, variant):
     if case["name"] == "witness":                                               # T7
         # kappa(A^{1/2}Z)^2 = kappa(G) = 1e20 >> 1/u: CHOLQR breaks down in its first Cholesky
         # (normal2 in pass 1); the pre-QR variant's A-stage is well conditioned (s8(c) item 14)
-        expect = 0 if variant == "prequr" else 1
+        expect = 0 if variant.startswith("prequr") else 1
         assert cls(st) == expect and cls(sto) == expect, (st, sto)
     else:
         assert st == 0 and sto == 0, (st, sto)
