@@ -156,7 +156,7 @@ def reference_arm(args, cfg, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"configs[{cfg}] oqr_{args.variant} m={m} n={n}; "
                                                     f"CPU oracle on leading {r}x{r} block",
                                         "m": m, "n": n},
