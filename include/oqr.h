@@ -35,7 +35,8 @@
  *              A-stage of oqr_prequr); the code is n + k (LAPACK xSYGV's INFO = N + i idiom).
  *    -i        argument i is invalid: -1 m, -2 n, -3 A (null or not 8-byte aligned), -4 lda
  *              (< m), -5 Z, -6 ldz, -7 Q, -8 R.  Nothing is launched.
- *   -100       a CUDA error occurred (launch or runtime); -101 workspace allocation failed.
+ *   -100       a CUDA error occurred (launch or runtime); -101 workspace allocation failed;
+ *   -102       caller-provided workspace too small or misaligned (async calls).
  *  On any nonzero status the contents of Q and R are unspecified.
  *
  * Preconditions that are NOT checked (reading R17): that A is SPD and
@@ -45,6 +46,7 @@
 #ifndef OQR_H
 #define OQR_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -138,6 +140,26 @@ int oqr_prequr_stable_sym(int64_t m, int64_t n, const double* A, int64_t lda, co
                           double* Q, double* R, oqr_stream_t stream);
 int oqr_prequr_stable_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z,
                               int64_t ldz, double* Q, double* R, oqr_stream_t stream);
+
+/*
+ * Asynchronous variants (CUDA-graph capturable).  Same computation as the synchronous calls, but
+ * nothing is synchronised: the call enqueues its kernels on `stream` and returns 0 (or a negative
+ * argument status, nothing enqueued); the factorisation status (0, k, n + k as above) is written to
+ * the device int *d_status when the stream reaches it.  workspace: caller-provided device memory of
+ * at least oqr_workspace_bytes(m, n) bytes, 256-byte aligned (then no allocation happens inside and
+ * the call can be captured into a CUDA graph), or NULL for a stream-ordered allocation from the
+ * library's pool.  Extra statuses: -9 d_status null, -102 workspace too small / misaligned.
+ */
+size_t oqr_workspace_bytes(int64_t m, int64_t n);
+int oqr_normal_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* Q,
+                     double* R, void* workspace, size_t workspace_bytes, int* d_status, oqr_stream_t stream);
+int oqr_normal2_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* Q,
+                      double* R, void* workspace, size_t workspace_bytes, int* d_status, oqr_stream_t stream);
+int oqr_prequr_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* Q,
+                     double* R, void* workspace, size_t workspace_bytes, int* d_status, oqr_stream_t stream);
+int oqr_prequr_stable_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                            double* Q, double* R, void* workspace, size_t workspace_bytes, int* d_status,
+                            oqr_stream_t stream);
 
 /* Human-readable text for a status code (static storage; never NULL). */
 const char* oqr_status_string(int status);

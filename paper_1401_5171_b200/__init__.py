@@ -24,7 +24,8 @@ __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm"
            "launch_count", "EXPORTS"]
 
 # Every symbol include/oqr.h declares.
-EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_prequr_stable", "oqr_prequr_stable_sym",
+EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_workspace_bytes", "oqr_normal_async",
+           "oqr_normal2_async", "oqr_prequr_async", "oqr_prequr_stable_async", "oqr_prequr_stable", "oqr_prequr_stable_sym",
            "oqr_prequr_stable_tridiag", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
            "oqr_gram_sym", "oqr_upload_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
@@ -63,6 +64,12 @@ def lib() -> ctypes.CDLL:
         L.oqr_gram_tridiag.argtypes = [I64, I64, P, P, P, I64, P, P]
         L.oqr_status_string.restype = ctypes.c_char_p
         L.oqr_status_string.argtypes = [I]
+        L.oqr_workspace_bytes.restype = ctypes.c_size_t
+        L.oqr_workspace_bytes.argtypes = [I64, I64]
+        for name in ("oqr_normal_async", "oqr_normal2_async", "oqr_prequr_async", "oqr_prequr_stable_async"):
+            f = getattr(L, name)
+            f.restype = I
+            f.argtypes = [I64, I64, P, I64, P, I64, P, P, P, ctypes.c_size_t, P, P]
         L.oqr_upload_sym.restype = I
         L.oqr_upload_sym.argtypes = [I64, P, I64, P, I64, P]
         L.oqr_gram_sym.restype = I
@@ -357,6 +364,44 @@ def trsm_rows(Z, R, r0: int, mr: int, Q=None, stream=None):
     if st:
         raise OqrError(st, "oqr_trsm")
     return Q
+
+
+def workspace_bytes(m: int, n: int) -> int:
+    """Bytes of caller workspace the *_async calls need (upper bound over all variants)."""
+    return int(lib().oqr_workspace_bytes(m, n))
+
+
+def _async(fname: str, A, Z, Q, R, workspace, status, stream=None):
+    m, n = A.shape[0], Z.shape[0]
+    ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else ctypes.c_void_p(None)
+    wsb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    st = getattr(lib(), fname)(m, n, _check(A, "A", m), A.shape[1], _check(Z, "Z", m), Z.shape[1],
+                               _check(Q, "Q", m), _check(R, "R", n), ws, wsb, ctypes.c_void_p(status.data_ptr()),
+                               _stream(stream))
+    if st:
+        raise OqrError(st, fname)
+
+
+def normal_async(A, Z, Q, R, workspace, status, stream=None):
+    """Enqueue CHOLQR without synchronising (CUDA-graph capturable with a workspace tensor of
+    workspace_bytes(m, n) bytes); the factorisation status lands in `status` (int32 CUDA tensor)."""
+    _async("oqr_normal_async", A, Z, Q, R, workspace, status, stream)
+
+
+def normal2_async(A, Z, Q, R, workspace, status, stream=None):
+    _async("oqr_normal2_async", A, Z, Q, R, workspace, status, stream)
+
+
+def prequr_async(A, Z, Q, R, workspace, status, stream=None):
+    _async("oqr_prequr_async", A, Z, Q, R, workspace, status, stream)
+
+
+def prequr_stable_async(A, Z, Q, R, workspace, status, stream=None):
+    _async("oqr_prequr_stable_async", A, Z, Q, R, workspace, status, stream)
+
+
+VARIANTS_ASYNC = {"normal": normal_async, "normal2": normal2_async, "prequr": prequr_async,
+                  "prequr_stable": prequr_stable_async}
 
 
 def timing_enable(on: bool = True):

@@ -64,8 +64,9 @@ static cudaMemPool_t library_pool() {
 // Stream-ordered scratch for one call.
 struct Workspace {
   double* base = nullptr;
+  bool owned = false;      // allocated from the library pool (freed stream-ordered at scope exit)
   double* Zp = nullptr;    // packed Z (or Q1 / Y)
-  double* Zc = nullptr;    // packed local rows of Z (row-sharded Gram only)
+  double* Zc = nullptr;    // packed local rows of Z / T Z / Z/2 (row-sharded, tridiagonal, symmetric)
   double* P = nullptr;     // per-CTA partial Gram slots
   double* G = nullptr;     // n x n Gram
   double* R1 = nullptr;    // n x n (R1 of normal2 / S of prequr)
@@ -74,21 +75,38 @@ struct Workspace {
   double* R4 = nullptr;    // n x n (stable pre-step: products)
   int* info = nullptr;
   cudaStream_t s = nullptr;
-  int alloc(int64_t m, int n, cudaStream_t st, int64_t mr_local = 0) {
+  static size_t doubles_for(int64_t m, int n, int64_t mr_local) {
+    const int NP = 8 * (int)cdiv(n, 8);
+    const size_t zp = (size_t)zp_doubles(m, NP);
+    const size_t zc = mr_local > 0 ? (size_t)zp_doubles(mr_local, NP) : 0;
+    const size_t sl = slots_doubles(n, gram_grid(m));
+    return zp + zc + sl + 5 * (size_t)n * n + 2;  // +2 doubles (16 B) for info
+  }
+  // user_ws: caller-provided workspace of user_bytes (no allocation: CUDA-graph capturable);
+  // user_info: device status word to use instead of the workspace's own.
+  int alloc(int64_t m, int n, cudaStream_t st, int64_t mr_local = 0, void* user_ws = nullptr,
+            size_t user_bytes = 0, int* user_info = nullptr) {
     s = st;
+    const size_t total = doubles_for(m, n, mr_local);
+    if (user_ws != nullptr) {
+      if (user_bytes < total * sizeof(double)) return -102;
+      if ((reinterpret_cast<uintptr_t>(user_ws) & 255) != 0) return -102;
+      base = static_cast<double*>(user_ws);
+    } else {
+      cudaMemPool_t pool = library_pool();
+      if (pool == nullptr ||
+          cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), total * sizeof(double), pool, st) != cudaSuccess) {
+        cudaGetLastError();
+        base = nullptr;
+        return -101;
+      }
+      owned = true;
+    }
     const int NP = 8 * (int)cdiv(n, 8);
     const size_t zp = (size_t)zp_doubles(m, NP);
     const size_t zc = mr_local > 0 ? (size_t)zp_doubles(mr_local, NP) : 0;
     const size_t sl = slots_doubles(n, gram_grid(m));
     const size_t nn = (size_t)n * n;
-    const size_t total = zp + zc + sl + 5 * nn + 2;  // +2 doubles (16 B) for info
-    cudaMemPool_t pool = library_pool();
-    if (pool == nullptr ||
-        cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), total * sizeof(double), pool, st) != cudaSuccess) {
-      cudaGetLastError();
-      base = nullptr;
-      return -101;
-    }
     Zp = base;
     Zc = Zp + zp;
     P = Zc + zc;
@@ -97,12 +115,19 @@ struct Workspace {
     R2 = R1 + nn;
     R3 = R2 + nn;
     R4 = R3 + nn;
-    info = reinterpret_cast<int*>(R4 + nn);
+    info = user_info ? user_info : reinterpret_cast<int*>(R4 + nn);
     return 0;
   }
   ~Workspace() {
-    if (base) cudaFreeAsync(base, s);
+    if (owned && base) cudaFreeAsync(base, s);
   }
+};
+
+// Asynchronous-call options: caller workspace (may be null: pool allocation) and device status.
+struct Async {
+  void* ws = nullptr;
+  size_t bytes = 0;
+  int* d_status = nullptr;
 };
 
 static int cuda_status(cudaError_t e) {
@@ -199,18 +224,20 @@ using namespace oqr;
 namespace oqr {
 
 static int run_normal(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
-                      cudaStream_t s) {
+                      cudaStream_t s, const Async* as = nullptr) {
   Workspace ws;
-  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
+  int st = as ? ws.alloc(m, n, s, m, as->ws, as->bytes, as->d_status)
+              : ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
   if (st) return st;
   if ((st = cholqr_pass(op, m, n, Z, ldz, Q, R, 0, ws, s))) return st;
-  return finish(ws, s);
+  return as ? 0 : finish(ws, s);
 }
 
 static int run_normal2(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
-                       cudaStream_t s) {
+                       cudaStream_t s, const Async* as = nullptr) {
   Workspace ws;
-  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
+  int st = as ? ws.alloc(m, n, s, m, as->ws, as->bytes, as->d_status)
+              : ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
   if (st) return st;
   // pass 1: [Q1, R1] = CHOLQR(A, Z), Q1 into Q
   if ((st = cholqr_pass(op, m, n, Z, ldz, Q, ws.R1, 0, ws, s))) return st;
@@ -218,13 +245,14 @@ static int run_normal2(const AOp& op, int64_t m, int n, const double* Z, int64_t
   if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
   // R = R2 R1
   if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R1, R, ws.info, s)))) return st;
-  return finish(ws, s);
+  return as ? 0 : finish(ws, s);
 }
 
 static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
-                      cudaStream_t s) {
+                      cudaStream_t s, const Async* as = nullptr) {
   Workspace ws;
-  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
+  int st = as ? ws.alloc(m, n, s, m, as->ws, as->bytes, as->d_status)
+              : ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
   if (st) return st;
   // pre-step: S = chol(Z^T Z), Y = Z S^{-1} (into Q)
   if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
@@ -234,16 +262,17 @@ static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t 
   if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
   // R = U S
   if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R1, R, ws.info, s)))) return st;
-  return finish(ws, s);
+  return as ? 0 : finish(ws, s);
 }
 
 // PRE-CHOLQR with the stable Euclidean pre-step (NEXT-N1, reading R21): shifted CholeskyQR3.
 //   G = Z^T Z, G += 11 (m n + n (n+1)) u tr(G) I, R1 = chol(G), Q1 = Z / R1 (into Q);
 //   two CholeskyQR passes on Q in place (R2, R3); S = R3 R2 R1; then [Q, U] = CHOLQR(A, Y); R = U S.
 static int run_prequr_stable(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
-                             cudaStream_t s) {
+                             cudaStream_t s, const Async* as = nullptr) {
   Workspace ws;
-  int st = ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
+  int st = as ? ws.alloc(m, n, s, m, as->ws, as->bytes, as->d_status)
+              : ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
   if (st) return st;
   const double factor = 11.0 * ((double)m * (double)n + (double)n * (double)(n + 1)) * 0x1.0p-53;
   if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
@@ -261,7 +290,7 @@ static int run_prequr_stable(const AOp& op, int64_t m, int n, const double* Z, i
   // A-stage: [Q, U] = CHOLQR(A, Y) in place (U into R2); breakdown code n + k
   if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
   if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R3, R, ws.info, s)))) return st;   // R = U S
-  return finish(ws, s);
+  return as ? 0 : finish(ws, s);
 }
 
 static AOp dense_op(const double* A, int64_t lda, bool sym = false) {
@@ -318,6 +347,51 @@ int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double*
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
   return run_prequr(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t oqr_workspace_bytes(int64_t m, int64_t n) {
+  if (m < 1 || n < 1 || n > m || n > OQR_NMAX) return 0;
+  return Workspace::doubles_for(m, (int)n, m) * sizeof(double);
+}
+
+static int async_call(int which, int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                      double* Q, double* R, void* ws, size_t ws_bytes, int* d_status, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  if (d_status == nullptr || !aligned(d_status, 4)) return -9;
+  Async as;
+  as.ws = ws;
+  as.bytes = ws_bytes;
+  as.d_status = d_status;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const AOp op = dense_op(A, lda);
+  switch (which) {
+    case 0: return run_normal(op, m, (int)n, Z, ldz, Q, R, s, &as);
+    case 1: return run_normal2(op, m, (int)n, Z, ldz, Q, R, s, &as);
+    case 2: return run_prequr(op, m, (int)n, Z, ldz, Q, R, s, &as);
+    default: return run_prequr_stable(op, m, (int)n, Z, ldz, Q, R, s, &as);
+  }
+}
+
+int oqr_normal_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* Q,
+                     double* R, void* workspace, size_t workspace_bytes, int* d_status, oqr_stream_t stream) {
+  return async_call(0, m, n, A, lda, Z, ldz, Q, R, workspace, workspace_bytes, d_status, stream);
+}
+
+int oqr_normal2_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* Q,
+                      double* R, void* workspace, size_t workspace_bytes, int* d_status, oqr_stream_t stream) {
+  return async_call(1, m, n, A, lda, Z, ldz, Q, R, workspace, workspace_bytes, d_status, stream);
+}
+
+int oqr_prequr_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz, double* Q,
+                     double* R, void* workspace, size_t workspace_bytes, int* d_status, oqr_stream_t stream) {
+  return async_call(2, m, n, A, lda, Z, ldz, Q, R, workspace, workspace_bytes, d_status, stream);
+}
+
+int oqr_prequr_stable_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                            double* Q, double* R, void* workspace, size_t workspace_bytes, int* d_status,
+                            oqr_stream_t stream) {
+  return async_call(3, m, n, A, lda, Z, ldz, Q, R, workspace, workspace_bytes, d_status, stream);
 }
 
 int oqr_prequr_stable(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
@@ -433,9 +507,10 @@ const char* oqr_status_string(int status) {
     case -6: return "invalid argument 6 (ldz < m)";
     case -7: return "invalid argument 7 (Q null or not 8-byte aligned)";
     case -8: return "invalid argument 8 (R null or not 8-byte aligned)";
-    case -9: return "invalid row range (r0 < 0, mr < 1 or r0 + mr > m)";
+    case -9: return "invalid argument: row range (oqr_gram_rows) or d_status (async calls)";
     case -100: return "CUDA error";
     case -101: return "workspace allocation failed";
+    case -102: return "caller workspace too small or not 256-byte aligned (see oqr_workspace_bytes)";
     default: return "unknown status";
   }
 }
