@@ -408,3 +408,24 @@ def test_prequr_stable_families(oqr, family):
     Qg, Rg = host(Q), host(R)
     assert A_orth(Qg) <= 10 * A_orth(Qo) + 1e-12
     assert oracle.componentwise_ratio(p.Z, Qg, Rg, p.m) <= 10 * oracle.componentwise_ratio(p.Z, Qo, Ro, p.m) + 4 * gamma(p.n + 1)
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_stable"])
+@pytest.mark.parametrize("mn", [(1, 1), (2, 2), (3, 1), (7, 3), (8, 8), (64, 64), (65, 1)])
+def test_tiny_shapes(oqr, variant, mn):
+    # the 64 x KS tensor-TMA box exceeds the whole matrix: rows/cols beyond m are zero-filled
+    m, n = mn
+    p = gen.problem(m, n, 10.0, 10.0, 81, lda=m + (m & 1))
+    Q, R, st = oqr.VARIANTS[variant](to_dev(p.A), to_dev(p.Z))
+    Qo, Ro, sto = oracle.VARIANTS[variant](p.A, p.Z, m)
+    assert st == sto == 0
+    Qg, Rg = host(Q), host(R)
+    assert np.allclose(Rg, Ro, rtol=1e-12, atol=1e-14 * np.abs(Ro).max())
+    assert np.allclose(Qg, Qo, rtol=1e-10, atol=1e-12 * np.abs(Qo).max())
+    if variant == "normal":
+        assert oracle.componentwise_ratio(p.Z, Qg, Rg, m) <= gamma(n + 1)
+    Gs = host(oqr.gram_sym(to_dev(p.A), to_dev(p.Z))).T
+    Go = oracle.from_cm(oracle.gram(p.A, p.Z, m), n)
+    Zd = np.abs(oracle.from_cm(p.Z, m))
+    M = Zd.T @ (np.abs(oracle.from_cm(p.A, m)) @ Zd)
+    assert np.all(np.abs(Gs - Go) <= 2 * gamma(3 * m) * M)

@@ -56,3 +56,16 @@ def test_eigenvector_closed_form():
     off = np.abs(Rd - np.diag(np.diag(Rd))).max()
     assert off <= 1e-9 * expect.max()
     assert oracle.orth_error_tridiag(d, e, Q, m) < 1e-9
+
+
+def test_dd_orth_tridiag_matches_dense_checker():
+    # the tridiagonal checker forms the same double-double sums as the dense one on the densified T
+    # (the dense one only adds exact zeros), so the rounded E agrees to far below u
+    m, n = 250, 9
+    d, e = gen.tridiag(m, 1e5)
+    p = gen.problem(m, n, 1e5, 1e3, 12, with_A=False)
+    Q, _, info = oracle.normal_tridiag(d, e, p.Z, m)
+    assert info == 0
+    Et = oracle.orth_error_tridiag(d, e, Q, m)
+    Ed = oracle.orth_error(oracle.densify_tridiag(d, e), Q, m)
+    assert abs(Et - Ed) <= 1e-6 * U * max(Ed, 1e-16) + 1e-30
