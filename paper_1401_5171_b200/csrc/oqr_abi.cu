@@ -21,6 +21,20 @@ static int64_t g_timing_total_launches0 = 0;
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+cudaError_t ensure_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> done;  // ((func, device), bytes)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& d : done)
+    if (d.first.first == func && d.first.second == dev && d.second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back({{func, dev}, bytes});
+  return e;
+}
+
 void timing_begin(cudaStream_t s) {
   if (!g_timing) return;
   if (g_event_used == g_events.size()) {

@@ -136,13 +136,8 @@ cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t
                          int info_off, cudaStream_t s, bool first) {
   const int NP = 8 * ((n + 7) / 8);
   const size_t bytes = (size_t)NP * (NP + 1) / 2 * sizeof(double);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_MAX - 1024);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(potrf_kernel), SMEM_MAX - 1024);
+  if (e != cudaSuccess) return e;
   potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off, first);
   note_launch();
   return cudaGetLastError();
@@ -329,13 +324,8 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   constexpr bool smem_rd = trsm_smem_doubles<NT>(true) * sizeof(double) <= (size_t)SMEM_MAX;
   constexpr size_t bytes = trsm_smem_doubles<NT>(smem_rd) * sizeof(double);
   static_assert(bytes <= (size_t)SMEM_MAX, "R fragments must fit in shared memory");
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(trsm_dmma_kernel<NT, smem_rd>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(trsm_dmma_kernel<NT, smem_rd>), (int)bytes);
+  if (e != cudaSuccess) return e;
   int64_t g = cdiv(m, (TRSM_THREADS / 32) * 8);  // 8 rows per warp per pass
   const int sms = trsm_num_sms();
   if (g > sms) g = sms;          // persistent: R is staged once per CTA

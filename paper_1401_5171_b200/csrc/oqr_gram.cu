@@ -749,12 +749,9 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
                                  const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s) {
   size_t bytes;
   const int stages = fused_stages(NT, &bytes);
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gram_fused_kernel<NT, SYM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_fused_kernel<NT, SYM>), (int)bytes);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   constexpr int KS = stage_k(NT);
   const int64_t KB = cdiv(m, KS), NPAN = cdiv(mr, BM);
@@ -789,12 +786,9 @@ static cudaError_t gram_packed_nt(int64_t m, const double* Xp, const double* Yp,
   int stages = (int)((SMEM_MAX - 256) / stage);
   if (stages > 8) stages = 8;
   const size_t bytes = 256 + stages * stage;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gram_packed_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bytes);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_packed_kernel<NT>), (int)bytes);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   const int64_t nblk = zp_blocks(m);
   int64_t nsl = num_sms() / NCP;

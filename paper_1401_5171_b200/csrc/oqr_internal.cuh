@@ -36,6 +36,8 @@ inline int64_t zp_doubles(int64_t m, int NP) { return zp_blocks(m) * (NP / 8) * 
 
 // ---- launch bookkeeping (oqr_abi.cu) ----
 void note_launch();
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device) -- thread-safe.
+cudaError_t ensure_smem_attr(const void* func, int bytes);
 void timing_begin(cudaStream_t s);
 void timing_end(cudaStream_t s);
 
