@@ -401,10 +401,18 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     double b_cur[NTL > 0 ? NTL : 1];
 #pragma unroll
     for (int t = 0; t < NTL; ++t) b_cur[t] = Zs[t * 4 * FRAG];
+    // the next k-step's fragments are prefetched while this one's DMMAs run -- except for
+    // NT > 25, where the second fragment set would not fit in 128 registers (spills)
+    constexpr bool PREFETCH = NT <= 25;
 #pragma unroll
     for (int kk = 0; kk < KS / 4; ++kk) {
       double a_nxt = 0.0, b_nxt[NTL > 0 ? NTL : 1];
-      if (kk + 1 < KS / 4) {
+      if (!PREFETCH && kk > 0) {
+        a_cur = As[kk * 4 * BM + a_off];
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) b_cur[t] = Zs[(((kk >> 2) * NT + t) * 4 + (kk & 3)) * FRAG];
+      }
+      if (PREFETCH && kk + 1 < KS / 4) {
         const int k1 = kk + 1, zb = k1 >> 2, k4 = k1 & 3;
         a_nxt = As[k1 * 4 * BM + a_off];
 #pragma unroll
@@ -412,7 +420,7 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
       }
 #pragma unroll
       for (int t = 0; t < NTL; ++t) dmma(acc[t], a_cur, b_cur[t]);
-      if (kk + 1 < KS / 4) {
+      if (PREFETCH && kk + 1 < KS / 4) {
         a_cur = a_nxt;
 #pragma unroll
         for (int t = 0; t < NTL; ++t) b_cur[t] = b_nxt[t];
