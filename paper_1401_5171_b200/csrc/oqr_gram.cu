@@ -183,7 +183,7 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
                                                int lane, int ctid) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
-  static_assert(NCH * LG * 64 == NCW * 32, "one chunk entry per thread");
+  static_assert(NCH * LG * 64 <= NCW * 32, "at most one chunk entry per thread");
 #ifdef OQR_EXP_NOCONTRACT  // experiment build only (tools/exp): measures the contraction's share
   {
     double t = 0.0;  // consume every accumulator (else ptxas drops the DMMAs)
@@ -214,7 +214,8 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
   const double* z1 = Zp + (((r1 / BK) * NT) * 4 + (r1 % BK) / 4) * FRAG + lane;
   constexpr int NG = (NTW + LG - 1) / LG;
   // this thread's entry of every chunk
-  const int vch = ctid >> 8, vj = (ctid >> 6) & (LG - 1), v64 = ctid & 63;
+  const bool has_entry = ctid < NCH * LG * 64;
+  const int vch = ctid / (LG * 64), vj = (ctid >> 6) % LG, v64 = ctid & 63;
   const int vt = v64 >> 1, ve = v64 & 1;
 #pragma unroll 1
   for (int kt = 0; kt < NT; ++kt) {
@@ -235,7 +236,7 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
       }
       const int tl = lg * LG + vj;
       const int lt = vch * NTW + tl;
-      const bool valid = tl < NTW && lt < NT;
+      const bool valid = has_entry && tl < NTW && lt < NT;
       double* p = slot + (int64_t)(lt * 8 + 2 * (vt & 3) + ve) * NP + kt * 8 + (vt >> 2);
       const double prev = (!first && valid) ? *p : 0.0;  // L2 latency overlaps the barrier
       __syncthreads();

@@ -17,7 +17,10 @@ constexpr int BK = 16;        // columns of A (k of AZ) per pipeline stage
 constexpr int NRG = 8;        // row groups per panel: 8 rows each (BM = 8 * NRG)
 constexpr int NCH = 2;        // column halves: warp (rg, ch) owns rows rg*8.. and half the n-tiles
 constexpr int NCW = NRG * NCH;  // 16 DMMA warps per CTA (4 per SM sub-partition)
-constexpr int LG = 4;         // n-tiles per warp per contraction chunk (reduction granule)
+#ifndef OQR_LG
+#define OQR_LG 4
+#endif
+constexpr int LG = OQR_LG;    // n-tiles per warp per contraction chunk (reduction granule)
 constexpr int NTMAX = 30;     // n <= 8 * NTMAX = 240 = OQR_NMAX
 constexpr int SMEM_MAX = 227 * 1024;
 constexpr int FRAG = 32;      // doubles per DMMA operand fragment (one per lane)
