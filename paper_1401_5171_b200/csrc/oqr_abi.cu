@@ -190,11 +190,14 @@ struct AOp {
 static int gram_into(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* G, Workspace& ws,
                      cudaStream_t s) {
   int g = 0;
-  OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
   if (op.tridiag) {
-    OQR_TRY(launch_pack_w_tridiag(m, n, op.d, op.e, Z, ldz, ws.Zc, s));
+    OQR_TRY(launch_pack_zw_tridiag(m, n, op.d, op.e, Z, ldz, ws.Zp, ws.Zc, s));
     OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zc, ws.P, &g, s));
-  } else if (op.sym) {
+    OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s, false));
+    return 0;
+  }
+  OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
+  if (op.sym) {
     OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zc, s, 0.5));  // Z / 2 (exact) for the diagonal panels
     OQR_TRY(launch_gram_fused(m, m, n, op.A, op.lda, ws.Zp, ws.Zp, ws.Zc, ws.P, &g, s));
   } else {

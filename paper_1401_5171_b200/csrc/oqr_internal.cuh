@@ -60,9 +60,9 @@ cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int
                               const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s);
 // G (n x n, ldg) = sum_{c<count} P_c, P_c = n x n (ld n) consecutive, c ascending.
 cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s);
-// W = T Z (T = tridiag(e, d, e)) packed like Zp.
-cudaError_t launch_pack_w_tridiag(int64_t m, int n, const double* d, const double* e, const double* Z, int64_t ldz,
-                                  double* Wp, cudaStream_t s);
+// Zp and W = T Z (T = tridiag(e, d, e)), both packed, in one pass over Z.
+cudaError_t launch_pack_zw_tridiag(int64_t m, int n, const double* d, const double* e, const double* Z, int64_t ldz,
+                                   double* Zp, double* Wp, cudaStream_t s);
 // Slots of X^T Y for two packed m x n operands (X = Y = Zp: the Euclidean Gram).
 cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
                                cudaStream_t s);
