@@ -318,8 +318,8 @@ def main():
         if os.path.exists(tp):
             try:
                 t = json.load(open(tp))
-                if t.get("m") == m and t.get("n") == n:
-                    traffic = t.get("dram_bytes_per_launch")
+                if t.get("m") == m and t.get("n") == n and world == 1 and not args.sharded:
+                    traffic = t["sym" if args.sym else "dense"]["dram_bytes_per_launch"]
             except Exception:
                 pass
         cpu = None
