@@ -16,7 +16,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # OQR_LIB overrides the library path (experiment builds under tools/exp only).
-LIB_PATH = os.environ.get("OQR_LIB", os.path.join(_HERE, "liboqr.so"))
+LIB_PATH = os.environ.get("OQR_LIB") or os.path.join(_HERE, "liboqr.so")
 NMAX = 240
 
 __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm", "status_string",

@@ -85,6 +85,22 @@ __device__ __forceinline__ void tma_g2s_2d(void* dst, const CUtensorMap* map, in
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_g2s_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                           uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_g2s_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                           uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -260,10 +276,24 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
 // has the k-blocks of the block-lower triangle including its own 64 x 64 diagonal panel,
 // nk(I) = min(KB, 4 (I + 1)), so the units before panel I number 2 I (I + 1) (only the last
 // panel can be clipped).
-// Stage width: 32 columns of A per stage when n <= 128 (NT <= 16: more DMMA work per stage to
-// amortise the per-stage hand-off), 16 otherwise (the 64 x 16 A tile + NT KiB of Z already fill
-// the ring).  The packed Z layout keeps 16-row blocks (BK); a 32-wide stage moves two of them.
-__host__ __device__ constexpr int stage_k(int NT) { return NT <= 16 ? 32 : 16; }
+// Stage width KS (columns of A per stage): every stage costs a fixed hand-off (barrier wait,
+// release, refill election), so wide stages pay -- 64 columns for n <= 64 (there K1 is HBM- or
+// hand-off-bound: 32 columns is 1.3x slower at n = 8..32), 32 above (16 is 2.5% slower at
+// n = 200 and 8% for the symmetric schedule, although a 32-wide ring holds only 2-3 stages
+// at n >= 200: tools/time_k1.py sweeps).  The packed Z layout keeps 16-row blocks
+// (BK); a KS-wide stage moves KS/16 of them.  OQR_EXP_KS_* override the thresholds (experiments).
+#ifndef OQR_EXP_KS_NT64
+#define OQR_EXP_KS_NT64 8
+#endif
+#ifndef OQR_EXP_KS_NT32
+#define OQR_EXP_KS_NT32 30
+#endif
+#ifndef OQR_EXP_PF32
+#define OQR_EXP_PF32 22
+#endif
+__host__ __device__ constexpr int stage_k(int NT) {
+  return NT <= OQR_EXP_KS_NT64 ? 64 : (NT <= OQR_EXP_KS_NT32 ? 32 : 16);
+}
 
 template <bool SYM, int KS>
 __host__ __device__ __forceinline__ int unit_nk(int I, int KB) {
@@ -317,6 +347,16 @@ __host__ __device__ __forceinline__ void unit_locate(int u, int KB, int* I, int*
   *kb = (int)(u - R * i * (i + 1) / 2);
 }
 
+// Shared-memory layouts of the 64 x KS A tile.  A warp's k-step reads rows rg*8 + 0..7 of four
+// columns, each half warp rows 0..3 or 4..7 of them.
+//  ALAY_R4  [row/4][col][row%4] (4-D tensor map): a half warp reads 16 consecutive doubles --
+//           conflict-free; TMA moves 32-byte lines.  The default (rows % 8 == 0).
+//  ALAY_R8  [row/8][col][row%8] (3-D map): 2-way bank conflict, 64-byte TMA lines.  n <= 8
+//           only, where K1 is HBM-bound and the line rate of the 32-byte layout, not shared
+//           memory, would limit it (tools/time_k1.py: 1.88 vs 2.15 ms at m = 40000, n = 8).
+//  ALAY_COL column-major 64 x KS (2-D map), 4-way conflict; rows % 8 != 0 only.
+constexpr int ALAY_COL = 0, ALAY_R8 = 1, ALAY_R4 = 2;
+
 // Fill a ring slot with unit (panel I, k-block kb): the A tile A[I*BM.., kb*KS..] (64 x KS,
 // column-major in smem) and the KS/16 packed Z blocks of the k-block (NT KiB each).  Executed by warp 0's lanes.
 // With a tensor map (A 16-byte aligned, lda even) both are single async requests and ragged
@@ -327,7 +367,7 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr
                                             const double* __restrict__ A, int64_t lda,
                                             const double* __restrict__ Zp, const double* __restrict__ Zh,
                                             double* As, uint64_t* bar, int lane, uint64_t pol_a, uint64_t pol_z,
-                                            bool tma_ok) {
+                                            bool tma_ok, int alay) {
   constexpr int ZB = KS / BK;                     // packed Z blocks per stage
   constexpr uint32_t zbytes = ZB * NT * 4 * FRAG * 8;
   constexpr uint32_t abytes = BM * KS * 8;
@@ -343,7 +383,9 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr
   if (tma_ok) {
     if (lane == 0) {
       mbar_arrive_expect_tx(bar, abytes + zbytes);
-      tma_g2s_2d(As, tmap, (int)row0, (int)col0, bar, pol_a);
+      if (alay == ALAY_R4) tma_g2s_4d(As, tmap, 0, (int)col0, 0, (int)(row0 >> 3), bar, pol_a);
+      else if (alay == ALAY_R8) tma_g2s_3d(As, tmap, 0, (int)col0, (int)(row0 >> 3), bar, pol_a);
+      else tma_g2s_2d(As, tmap, (int)row0, (int)col0, bar, pol_a);
       bulk_g2s(Zs, zsrc, zbytes, bar, pol_z);
     }
   } else {
@@ -351,7 +393,8 @@ __device__ __forceinline__ void issue_stage(int I, int kb, int64_t m, int64_t mr
       const int k = e / BM, r = e - k * BM;
       double v = 0.0;
       if (row0 + r < mr && col0 + k < m) v = A[(col0 + k) * lda + row0 + r];
-      As[e] = v;
+      As[alay == ALAY_R4 ? (((r >> 2) * KS + k) << 2) + (r & 3)
+                         : (alay == ALAY_R8 ? (((r >> 3) * KS + k) << 3) + (r & 7) : e)] = v;
     }
     fence_proxy_async_smem();  // generic writes before later async-proxy writes to the slot
     __syncwarp();
@@ -374,7 +417,7 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
                                               const double* __restrict__ Zh, double* slot,
                                               double* red, double* ring, uint64_t* full, uint64_t* empty,
                                               unsigned* relcnt, int KB, int u0, int u1, int stages,
-                                              bool tma_ok, int rg, int ch, int lane, uint64_t pol_a,
+                                              bool tma_ok, int alay, int rg, int ch, int lane, uint64_t pol_a,
                                               uint64_t pol_z) {
   constexpr int NTW = (NT + 1) / 2;
   constexpr int ZB = KS / BK;
@@ -393,10 +436,17 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
   int Ii, kbi;
   unit_locate<SYM, KS>(ui, KB, &Ii, &kbi);
   int nki = unit_nk<SYM, KS>(Ii, KB);
-  // A fragment: A[row0 + rg*8 + lane/4, col0 + kk*4 + lane%4] from the column-major 64 x 16 tile
-  const int a_off = (lane & 3) * BM + rg * 8 + (lane >> 2);
+  // A fragment: A[row0 + rg*8 + lane/4, col0 + kk*4 + lane%4] (tile layouts: see ALAY_*)
+  const int a_off = alay == ALAY_R4   ? (((2 * rg + (lane >> 4)) * KS + (lane & 3)) << 2) + ((lane >> 2) & 3)
+                    : alay == ALAY_R8 ? ((rg * KS + (lane & 3)) << 3) + (lane >> 2)
+                                      : (lane & 3) * BM + rg * 8 + (lane >> 2);
+  const int a_step = alay == ALAY_R4 ? 16 : (alay == ALAY_R8 ? 32 : 4 * BM);  // doubles per k-step
   // B fragment (block zb, lt, kk): 32 consecutive doubles of the packed blocks
   const int b_off = BM * KS + ch * NTW * 4 * FRAG + lane;
+  unsigned pend = 0u;  // lane 0: the previous release's counter value (elects the refiller)
+  bool pvalid = false;
+  int ps = 0, pIi = 0, pkbi = 0;
+  uint32_t pph = 0;
   for (int u = u0; u < u1; ++u) {
     mbar_wait(&full[s], ph);
     const double* As = ring + s * STAGE;
@@ -406,19 +456,20 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
 #pragma unroll
     for (int t = 0; t < NTL; ++t) b_cur[t] = Zs[t * 4 * FRAG];
     // the next k-step's fragments are prefetched while this one's DMMAs run -- except for
-    // NT > 25, where the second fragment set would not fit in 128 registers (spills)
-    constexpr bool PREFETCH = NT <= 25;
+    // NT > 22 (KS = 32; 25 for KS = 16), where the second fragment set does not fit in 128
+    // registers next to the accumulators (spills)
+    constexpr bool PREFETCH = NT <= (KS == 16 ? 25 : OQR_EXP_PF32);
 #pragma unroll
     for (int kk = 0; kk < KS / 4; ++kk) {
       double a_nxt = 0.0, b_nxt[NTL > 0 ? NTL : 1];
       if (!PREFETCH && kk > 0) {
-        a_cur = As[kk * 4 * BM + a_off];
+        a_cur = As[kk * a_step + a_off];
 #pragma unroll
         for (int t = 0; t < NTL; ++t) b_cur[t] = Zs[(((kk >> 2) * NT + t) * 4 + (kk & 3)) * FRAG];
       }
       if (PREFETCH && kk + 1 < KS / 4) {
         const int k1 = kk + 1, zb = k1 >> 2, k4 = k1 & 3;
-        a_nxt = As[k1 * 4 * BM + a_off];
+        a_nxt = As[k1 * a_step + a_off];
 #pragma unroll
         for (int t = 0; t < NTL; ++t) b_nxt[t] = Zs[((zb * NT + t) * 4 + k4) * FRAG];
       }
@@ -430,20 +481,44 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
         for (int t = 0; t < NTL; ++t) b_cur[t] = b_nxt[t];
       }
     }
-    __syncwarp();
-    // release the slot; the LAST warp to release it refills it at once (no warp is paced by
-    // another's compute).  The arrival counter only elects that warp; the empty mbarrier's
-    // acquire then orders all warps' reads of the slot before the new async writes.
-    int last = 0;
-    if (lane == 0) {
-      mbar_arrive(&empty[s]);
-      last = (atomicAdd(&relcnt[s], 1u) % NCW) == NCW - 1;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && ui < u1) {
-      mbar_wait(&empty[s], ph);
-      issue_stage<NT, SYM, KS>(Ii, kbi, m, mr, tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a,
-                               pol_z, tma_ok);
+    // Release the slot; the LAST warp to release it refills it (no warp is paced by another's
+    // compute).  The arrival counter only elects that warp; the empty mbarrier's acquire then
+    // orders all warps' reads of the slot before the new async writes.  The election result is
+    // read one unit later (after this warp's next DMMAs are issued), so the counter's round
+    // trip is off the per-unit critical path; the refill lands stages - 2 units ahead.  Only for
+    // NT <= 16 (short stages, where that round trip matters): the five extra live registers
+    // would make the NT > 22 instantiations spill.
+    constexpr bool DEFER = NT <= 16;
+    if (!DEFER) {
+      __syncwarp();
+      unsigned cnt = 0u;
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        cnt = atomicAdd(&relcnt[s], 1u);
+      }
+      cnt = __shfl_sync(0xffffffffu, cnt, 0);
+      if ((cnt % NCW) == NCW - 1 && ui < u1) {
+        mbar_wait(&empty[s], ph);
+        issue_stage<NT, SYM, KS>(Ii, kbi, m, mr, tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a,
+                                 pol_z, tma_ok, alay);
+      }
+    } else {
+      const unsigned prev = __shfl_sync(0xffffffffu, pend, 0);
+      if (pvalid && (prev % NCW) == NCW - 1) {
+        mbar_wait(&empty[ps], pph);
+        issue_stage<NT, SYM, KS>(pIi, pkbi, m, mr, tmap, A, lda, Zp, Zh, ring + ps * STAGE, &full[ps], lane, pol_a,
+                                 pol_z, tma_ok, alay);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        pend = atomicAdd(&relcnt[s], 1u);
+      }
+      pvalid = ui < u1;
+      ps = s;
+      pph = ph;
+      pIi = Ii;
+      pkbi = kbi;
     }
     ++ui;
     if (++kbi == nki) {
@@ -479,7 +554,7 @@ template <int NT, bool SYM>
 __global__ void __launch_bounds__(NCW * 32, 1)
 gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t mr, const double* __restrict__ A,
                   int64_t lda, const double* __restrict__ Zp, const double* __restrict__ Zc,
-                  const double* __restrict__ Zh, double* __restrict__ P, int KB, int U, int stages, bool tma_ok,
+                  const double* __restrict__ Zh, double* __restrict__ P, int KB, int U, int stages, bool tma_ok, int alay,
                   double panel_w) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
@@ -522,16 +597,16 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
       int I, kb;
       unit_locate<SYM, KS>(u0 + s, KB, &I, &kb);
       issue_stage<NT, SYM, KS>(I, kb, m, mr, &tmap, A, lda, Zp, Zh, ring + s * STAGE, &full[s], lane, pol_a, pol_z,
-                               tma_ok);
+                               tma_ok, alay);
     }
   }
   double* slot = P + c * (int64_t)NP * NP;
   if (ch == 0)
     consume_units<NT, NTW, SYM, KS>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB, u0,
-                                u1, stages, tma_ok, rg, ch, lane, pol_a, pol_z);
+                                u1, stages, tma_ok, alay, rg, ch, lane, pol_a, pol_z);
   else
     consume_units<NT, NT - NTW, SYM, KS>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB,
-                                     u0, u1, stages, tma_ok, rg, ch, lane, pol_a, pol_z);
+                                     u0, u1, stages, tma_ok, alay, rg, ch, lane, pol_a, pol_z);
 }
 
 // ------------------------------------------------------------------ K4' -------------------
@@ -743,10 +818,32 @@ static EncodeTiledFn encode_fn() {
 // A (or a row block of it) as a 2-D FP64 tensor {rows mr (contiguous), cols m (stride lda)},
 // box {BM, KS}, no swizzle,
 // out-of-bounds elements zero-filled.
-static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t mr, int64_t m, int64_t lda, int ks) {
+// The A tensor map for tile layout alay (ALAY_*): ALAY_R4 is the 4-D view (row % 4, col,
+// (row / 4) % 2, row / 8) of the same matrix, strides {8 B, lda * 8 B, 32 B, 64 B} (not
+// increasing -- the encoder accepts that, tools/tma3d_probe.cu), box (4, ks, 2, 8); ALAY_R8 the
+// 3-D view (row % 8, col, row / 8), box (8, ks, 8); ALAY_COL the plain 2-D view, box (64, ks).
+static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t mr, int64_t m, int64_t lda, int ks, int alay) {
   if ((reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0 || m > (int64_t)INT32_MAX) return false;
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
+  if (alay == ALAY_R8) {
+    const cuuint64_t dims[3] = {8, (cuuint64_t)m, (cuuint64_t)(mr / 8)};
+    const cuuint64_t strides[2] = {(cuuint64_t)lda * sizeof(double), 8 * sizeof(double)};
+    const cuuint32_t box[3] = {8, (cuuint32_t)ks, (cuuint32_t)(BM / 8)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(A), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (alay == ALAY_R4) {
+    const cuuint64_t dims[4] = {4, (cuuint64_t)m, 2, (cuuint64_t)(mr / 8)};
+    const cuuint64_t strides[3] = {(cuuint64_t)lda * sizeof(double), 4 * sizeof(double), 8 * sizeof(double)};
+    const cuuint32_t box[4] = {4, (cuuint32_t)ks, 2, (cuuint32_t)(BM / 8)};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(A), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   const cuuint64_t dims[2] = {(cuuint64_t)mr, (cuuint64_t)m};
   const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
   const cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)ks};
@@ -776,13 +873,14 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
   *g_out = (int)g;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda, KS);
+  const int alay = (mr % 8) != 0 ? ALAY_COL : (NT == 1 ? ALAY_R8 : ALAY_R4);
+  const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda, KS, alay);
   timing_begin(s);
   static const char* env_w = getenv("OQR_PANEL_W");
   // panel weight in units: a unit carries KS/16 times the work of a 16-wide unit
   const double panel_w = env_w ? atof(env_w) : PANEL_W_PER_NT * NT * (16.0 / KS);
   gram_fused_kernel<NT, SYM><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, Zh, P, (int)KB,
-                                                                  (int)U, stages, tma_ok, panel_w);
+                                                                  (int)U, stages, tma_ok, alay, panel_w);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);

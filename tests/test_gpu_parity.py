@@ -201,6 +201,21 @@ def outcome_determined(p, variant):
     return ok
 
 
+def cholqr_orth_bound(p, Qo, Ro):
+    """Theorem 2, eq. (orth1) with c = 1, evaluated on the oracle's factors:
+    ||Q^T A Q - I|| <= m n u ||R^-1|| ||Z|| (||R^-1|| ||A Z|| + ||Q|| ||A||).  Where this exceeds
+    10 E_orc (orthogonality essentially lost: u kappa(G) near 1) the two results differ by
+    rounding alone and the theorem is the only claim the paper makes about either."""
+    m, n = p.m, p.n
+    Z, Q, R = oracle.from_cm(p.Z, m), oracle.from_cm(Qo, m), oracle.from_cm(Ro, n)
+    A = p.A[:m, :m]
+    smin = np.linalg.svd(R, compute_uv=False)[-1]
+    if smin == 0:
+        return math.inf
+    nrm = lambda X: np.linalg.norm(X, 2)
+    return m * n * U * nrm(Z) / smin * (nrm(A @ Z) / smin + nrm(Q) * float(np.max(p.d)))
+
+
 def variant_gates(oqr, p, variant, family="dense"):
     m, n = p.m, p.n
     fams = {"dense": oqr.VARIANTS, "sym": oqr.VARIANTS_SYM}
@@ -230,7 +245,10 @@ def variant_gates(oqr, p, variant, family="dense"):
     eo = oracle.orth_error(p.A, Qo, m)
     normA = float(np.max(p.d))                                  # ||A||_2 (generator ground truth)
     normQ = np.linalg.norm(oracle.from_cm(Qo, m), 2)
-    assert e <= 10 * eo + 10 * n * U * normA * normQ ** 2, (e, eo)
+    tol = 10 * eo + 10 * n * U * normA * normQ ** 2
+    if variant == "normal":
+        tol = max(tol, cholqr_orth_bound(p, Qo, Ro))
+    assert e <= tol, (e, eo, tol)
     G = oracle.from_cm(oracle.gram(p.A, p.Z, m), n)             # T6
     tol_R, tol_Q = forward_tols(p, G, Ro, Qo)
     assert np.linalg.norm(Rg - Ro) <= tol_R, (np.linalg.norm(Rg - Ro), tol_R)

@@ -1,5 +1,5 @@
 """Per-step CUDA-event timings through the step exports (pack+K1+K1r, K2, K3) and the three
-variants, for one BASELINE config.      python tools/time_steps.py [config] [reps]"""
+variants, for one BASELINE config (or "m,n").      python tools/time_steps.py [config|m,n] [reps]"""
 import os
 import sys
 
@@ -38,8 +38,11 @@ if cfg in gen.TRIDIAG_CONFIGS:
     print(f"tridiag config {cfg} m={m} n={n}: " + ", ".join(f"{k} {v:.4f} ms" for k, v in res.items()) +
           f"; normal {fl / res['normal'] / 1e9:.2f} TFLOP/s (2mn^2 normalisation)")
     sys.exit(0)
-cfg = int(cfg)
-p = gen.config(cfg)
+if "," in cfg:                       # "m,n": a synthetic problem off the BASELINE list
+    mm, nn = (int(x) for x in cfg.split(","))
+    p = gen.problem(mm, nn, 1e3, 1e2, 7)
+else:
+    p = gen.config(int(cfg))
 m, n = p.m, p.n
 A = torch.from_numpy(p.A).cuda()
 Z = torch.from_numpy(p.Z).cuda()
@@ -61,7 +64,10 @@ G = oqr.gram(A, Z)
 R, info = oqr.potrf(G)
 torch.cuda.synchronize()
 assert int(info.item()) == 0
+oqr.timing_enable(True)
+oqr.timing_reset()
 res = {"gram (pack+K1+K1r)": timed(lambda: oqr.gram(A, Z, G)),
+       "K1 alone": (lambda t: t[0] / t[1])(oqr.timing_read()),
        "gram_euclid (pack+K4+K1r)": timed(lambda: oqr.gram_euclid(Z, m=m)),
        "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)),
        "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
