@@ -69,13 +69,23 @@ def summary(rep, name, title):
 d = summary(os.path.join(G, "k1_c3.ncu-rep"), f"{tag}_k1_c3_ncu_summary.txt",
             f"# {tag} K1 gram_fused_kernel<25, dense> (ncu --set full --clock-control none), m=40000 n=200; "
             "command: python tools/prof_k1.py 40000 200 2 (-k regex:gram_fused -s 1 -c 1)")
-tb = float(d["dram__bytes_read.sum"][0]) * MULT[d["dram__bytes_read.sum"][1]] + \
-    float(d["dram__bytes_write.sum"][0]) * MULT[d["dram__bytes_write.sum"][1]]
-json.dump({"m": 40000, "n": 200, "kernel": "gram_fused_kernel<25, dense>", "dram_bytes_per_launch": tb,
-           "algorithmic_bytes_per_launch": 8 * 40000 ** 2,
-           "source": f"profiles/{tag}_k1_c3_ncu_summary.txt (ncu --set full)"},
-          open(os.path.join(P, "k1_traffic.json"), "w"), indent=1)
+
+
+def dram_bytes(d):
+    return sum(float(d[k][0]) * MULT[d[k][1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+
+
+traffic = {"m": 40000, "n": 200,
+           "dense": {"kernel": "gram_fused_kernel<25, dense>", "dram_bytes_per_launch": dram_bytes(d),
+                     "algorithmic_bytes_per_launch": 8 * 40000 ** 2,
+                     "source": f"profiles/{tag}_k1_c3_ncu_summary.txt (ncu --set full)"}}
 if os.path.exists(os.path.join(G, "k1sym_c3.ncu-rep")):
-    summary(os.path.join(G, "k1sym_c3.ncu-rep"), f"{tag}_k1sym_c3_ncu_summary.txt",
-            f"# {tag} K1 gram_fused_kernel<25, sym> (block-lower triangle), m=40000 n=200; "
-            "command: python tools/time_k1.py 40000 200 1 sym (-k regex:gram_fused -s 1 -c 1)")
+    ds = summary(os.path.join(G, "k1sym_c3.ncu-rep"), f"{tag}_k1sym_c3_ncu_summary.txt",
+                 f"# {tag} K1 gram_fused_kernel<25, sym> (block-lower triangle), m=40000 n=200; "
+                 "command: python tools/time_k1.py 40000 200 1 sym (-k regex:gram_fused -s 1 -c 1)")
+    P64 = 40000 // 64
+    traffic["sym"] = {"kernel": "gram_fused_kernel<25, sym> (block-lower triangle of A)",
+                      "dram_bytes_per_launch": dram_bytes(ds),
+                      "algorithmic_bytes_per_launch": 8 * 64 * 64 * P64 * (P64 + 1) // 2,
+                      "source": f"profiles/{tag}_k1sym_c3_ncu_summary.txt (ncu --set full)"}
+json.dump(traffic, open(os.path.join(P, "k1_traffic.json"), "w"), indent=1)
