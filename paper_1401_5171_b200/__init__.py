@@ -21,10 +21,10 @@ NMAX = 240
 
 __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm", "status_string",
            "OqrError", "lib", "LIB_PATH", "NMAX", "timing_enable", "timing_reset", "timing_read",
-           "launch_count", "EXPORTS"]
+           "launch_count", "EXPORTS", "normal_host"]
 
 # Every symbol include/oqr.h declares.
-EXPORTS = ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_workspace_bytes", "oqr_normal_async",
+EXPORTS = ("oqr_normal", "oqr_normal_host", "oqr_normal2", "oqr_prequr", "oqr_workspace_bytes", "oqr_normal_async",
            "oqr_normal2_async", "oqr_prequr_async", "oqr_prequr_stable_async", "oqr_prequr_stable", "oqr_prequr_stable_sym",
            "oqr_prequr_stable_tridiag", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
            "oqr_gram_sym", "oqr_upload_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
@@ -70,6 +70,8 @@ def lib() -> ctypes.CDLL:
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, I64, P, I64, P, P, P, ctypes.c_size_t, P, P]
+        L.oqr_normal_host.restype = I
+        L.oqr_normal_host.argtypes = [I64, I64, P, I64, P, I64, P, P, I64, P]
         L.oqr_upload_sym.restype = I
         L.oqr_upload_sym.argtypes = [I64, P, I64, P, I64, P]
         L.oqr_gram_sym.restype = I
@@ -145,6 +147,37 @@ def normal(A, Z, Q=None, R=None, stream=None, check: bool = True):
     """CHOLQR, Algorithm 1.  Returns (Q, R, status); status > 0 is a
     Cholesky breakdown (see include/oqr.h), negative statuses raise unless check=False."""
     return _variant("oqr_normal", A, Z, Q, R, stream, check)
+
+
+def _host(t, name: str, rows: int):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or t.is_cuda:
+        raise TypeError(f"{name}: expected a float64 CPU tensor")
+    if t.dim() != 2 or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous 2-D tensor of shape (cols, ld)")
+    if t.shape[1] < rows:
+        raise ValueError(f"{name}: leading dimension {t.shape[1]} < {rows}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def normal_host(A, Z, Q=None, R=None, chunk_cols: int = 0, stream=None, check: bool = True):
+    """oqr_normal on HOST tensors (pinned for full PCIe bandwidth and copy/compute overlap):
+    A is staged to the device in column chunks while the fused Gram runs on the chunks already
+    there (include/oqr.h).  Returns host (Q, R, status)."""
+    import torch
+    m, n = A.shape[0], Z.shape[0]
+    pin = A.is_pinned()
+    if Q is None:
+        Q = torch.empty((n, m), dtype=torch.float64, pin_memory=pin)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, pin_memory=pin)
+    if Q.shape != (n, m) or R.shape != (n, n):
+        raise ValueError("Q must be (n, m) and R (n, n)")
+    st = lib().oqr_normal_host(m, n, _host(A, "A", m), A.shape[1], _host(Z, "Z", m), Z.shape[1], _host(Q, "Q", m),
+                               _host(R, "R", n), int(chunk_cols), _stream(stream))
+    if check and st < 0:
+        raise OqrError(st, "oqr_normal_host")
+    return Q, R, st
 
 
 def normal2(A, Z, Q=None, R=None, stream=None, check: bool = True):

@@ -2,6 +2,7 @@
 //
 // Host-side orchestration only: argument checks, stream-ordered workspace, kernel launches on
 // the caller's stream, the status read-back.  Every arithmetic step runs in a kernel.
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -282,6 +283,74 @@ static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t 
   return as ? 0 : finish(ws, s);
 }
 
+// oqr_normal on host arrays: A moves to the device in column chunks on a copy stream while the
+// fused Gram of the chunks already landed runs on `s` (G = sum_J Z^T A[:, J] Z[J, :], every chunk
+// accumulating into the same per-CTA slots, chunk order fixed), then K1r, K2, K3 and the copies
+// of Q, R back.  Device A (even leading dimension, TMA-aligned), Z, Q come from the library pool.
+static int run_normal_host(int64_t m, int n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                           double* Q, double* R, int64_t chunk_cols, cudaStream_t s) {
+  Workspace ws;
+  int st = ws.alloc(m, n, s);
+  if (st) return st;
+  const int64_t ldd = m + (m & 1);
+  const size_t dbytes = ((size_t)ldd * (size_t)m + 2 * (size_t)m * (size_t)n) * sizeof(double);
+  double* buf = nullptr;
+  cudaMemPool_t pool = library_pool();
+  if (pool == nullptr || cudaMallocFromPoolAsync(reinterpret_cast<void**>(&buf), dbytes, pool, s) != cudaSuccess) {
+    cudaGetLastError();
+    return -101;
+  }
+  double* Ad = buf;
+  double* Zd = Ad + (size_t)ldd * (size_t)m;
+  double* Qd = Zd + (size_t)m * (size_t)n;
+  int64_t chunk = chunk_cols > 0 ? chunk_cols : cdiv(m, 8);
+  chunk = cdiv(chunk, BM) * BM;
+  const int64_t nchunks = cdiv(m, chunk);
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> ev((size_t)nchunks + 1, nullptr);
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  for (auto& x : ev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  // the copy stream starts after the pool allocation (stream-ordered on s)
+  if (e == cudaSuccess) e = cudaEventRecord(ev[nchunks], s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[nchunks], 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(Zd, (size_t)m * 8, Z, (size_t)ldz * 8, (size_t)m * 8, (size_t)n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_pack_z(m, n, Zd, m, ws.Zp, s);
+  const int NT = (int)cdiv(n, 8);
+  int g0 = 0;
+  for (int64_t j = 0; j < nchunks && e == cudaSuccess; ++j) {
+    const int64_t c0 = j * chunk, w = std::min(chunk, m - c0);
+    e = cudaMemcpy2DAsync(Ad + c0 * ldd, (size_t)ldd * 8, A + c0 * lda, (size_t)lda * 8, (size_t)m * 8, (size_t)w,
+                          cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[j], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[j], 0);
+    int g = 0;
+    // chunk columns c0.. are k-blocks of Z rows c0.. (packed blocks of 16 rows; c0 % 64 == 0);
+    // the contraction operand is all of Z
+    if (e == cudaSuccess)
+      e = launch_gram_fused(w, m, n, Ad + c0 * ldd, ldd, ws.Zp + (c0 / BK) * NT * 4 * FRAG, ws.Zp, nullptr, ws.P, &g,
+                            s, j > 0);
+    if (j == 0) g0 = g;
+  }
+  if (e == cudaSuccess) e = launch_gram_reduce(n, g0, ws.P, ws.G, n, s, false);
+  if (e == cudaSuccess) e = launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true);
+  if (e == cudaSuccess) e = launch_trsm(m, n, Zd, m, ws.R1, n, Qd, m, ws.info, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(Q, Qd, (size_t)m * (size_t)n * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(R, ws.R1, (size_t)n * (size_t)n * 8, cudaMemcpyDeviceToHost, s);
+  int info = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&info, ws.info, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(buf, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  else cudaStreamSynchronize(s);
+  for (auto& x : ev)
+    if (x) cudaEventDestroy(x);
+  if (cs) cudaStreamDestroy(cs);
+  if (e != cudaSuccess) return cuda_status(e);
+  return info;
+}
+
 // PRE-CHOLQR with the stable Euclidean pre-step (NEXT-N1, reading R21): shifted CholeskyQR3.
 //   G = Z^T Z, G += 11 (m n + n (n+1)) u tr(G) I, R1 = chol(G), Q1 = Z / R1 (into Q);
 //   two CholeskyQR passes on Q in place (R2, R3); S = R3 R2 R1; then [Q, U] = CHOLQR(A, Y); R = U S.
@@ -357,6 +426,14 @@ int oqr_normal2(int64_t m, int64_t n, const double* A, int64_t lda, const double
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
   return run_normal2(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_normal_host(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                    double* Q, double* R, int64_t chunk_cols, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  if (chunk_cols < 0) return -9;
+  return run_normal_host(m, (int)n, A, lda, Z, ldz, Q, R, chunk_cols, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
@@ -524,7 +601,7 @@ const char* oqr_status_string(int status) {
     case -6: return "invalid argument 6 (ldz < m)";
     case -7: return "invalid argument 7 (Q null or not 8-byte aligned)";
     case -8: return "invalid argument 8 (R null or not 8-byte aligned)";
-    case -9: return "invalid argument: row range (oqr_gram_rows) or d_status (async calls)";
+    case -9: return "invalid argument: row range (oqr_gram_rows), d_status (async calls) or chunk_cols (oqr_normal_host)";
     case -100: return "CUDA error";
     case -101: return "workspace allocation failed";
     case -102: return "caller workspace too small or not 256-byte aligned (see oqr_workspace_bytes)";

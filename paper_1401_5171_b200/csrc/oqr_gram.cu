@@ -417,8 +417,8 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
                                               const double* __restrict__ Zh, double* slot,
                                               double* red, double* ring, uint64_t* full, uint64_t* empty,
                                               unsigned* relcnt, int KB, int u0, int u1, int stages,
-                                              bool tma_ok, int alay, int rg, int ch, int lane, uint64_t pol_a,
-                                              uint64_t pol_z) {
+                                              bool tma_ok, int alay, bool accum, int rg, int ch, int lane,
+                                              uint64_t pol_a, uint64_t pol_z) {
   constexpr int NTW = (NT + 1) / 2;
   constexpr int ZB = KS / BK;
   constexpr int STAGE = BM * KS + ZB * NT * 4 * FRAG;
@@ -426,7 +426,7 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
   double acc[NTW][2];
 #pragma unroll
   for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
-  bool first = true;
+  bool first = !accum;  // accum: the slot already holds an earlier launch's partial (column chunks)
   int s = 0;
   uint32_t ph = 0;
   int I, kb;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(NCW * 32, 1)
 gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t mr, const double* __restrict__ A,
                   int64_t lda, const double* __restrict__ Zp, const double* __restrict__ Zc,
                   const double* __restrict__ Zh, double* __restrict__ P, int KB, int U, int stages, bool tma_ok, int alay,
-                  double panel_w) {
+                  double panel_w, bool accum) {
   constexpr int NP = NT * 8;
   constexpr int NTW = (NT + 1) / 2;
   constexpr int KS = stage_k(NT);
@@ -575,7 +575,8 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
   const int u1 = unit_split<SYM, KS>(c + 1, g, U, KB, npanels, panel_w);
   if (u0 >= u1) {  // the weighted split can leave a CTA without units: its slot is zero
     double* slot = P + c * (int64_t)NP * NP;
-    for (int e = threadIdx.x; e < NP * NP; e += blockDim.x) slot[e] = 0.0;
+    if (!accum)
+      for (int e = threadIdx.x; e < NP * NP; e += blockDim.x) slot[e] = 0.0;
     return;
   }
 
@@ -603,10 +604,10 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
   double* slot = P + c * (int64_t)NP * NP;
   if (ch == 0)
     consume_units<NT, NTW, SYM, KS>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB, u0,
-                                u1, stages, tma_ok, alay, rg, ch, lane, pol_a, pol_z);
+                                u1, stages, tma_ok, alay, accum, rg, ch, lane, pol_a, pol_z);
   else
     consume_units<NT, NT - NTW, SYM, KS>(&tmap, m, mr, A, lda, Zp, Zc, Zh, slot, red, ring, full, empty, relcnt, KB,
-                                     u0, u1, stages, tma_ok, alay, rg, ch, lane, pol_a, pol_z);
+                                     u0, u1, stages, tma_ok, alay, accum, rg, ch, lane, pol_a, pol_z);
 }
 
 // ------------------------------------------------------------------ K4' -------------------
@@ -855,7 +856,8 @@ static bool make_tmap_a(CUtensorMap* map, const double* A, int64_t mr, int64_t m
 
 template <int NT, bool SYM>
 static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t lda, const double* Zp,
-                                 const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s) {
+                                 const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s,
+                                 bool accum) {
   size_t bytes;
   const int stages = fused_stages(NT, &bytes);
   {
@@ -880,7 +882,7 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
   // panel weight in units: a unit carries KS/16 times the work of a 16-wide unit
   const double panel_w = env_w ? atof(env_w) : PANEL_W_PER_NT * NT * (16.0 / KS);
   gram_fused_kernel<NT, SYM><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, Zh, P, (int)KB,
-                                                                  (int)U, stages, tma_ok, alay, panel_w);
+                                                                  (int)U, stages, tma_ok, alay, panel_w, accum);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);
@@ -914,13 +916,14 @@ static cudaError_t gram_packed_nt(int64_t m, const double* Xp, const double* Yp,
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
 
 cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int64_t lda, const double* Zp,
-                              const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s) {
+                              const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s,
+                              bool accum) {
   if (Zh != nullptr && mr != m) return cudaErrorInvalidValue;  // SYM is a whole-matrix schedule
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT)                                                                        \
   case NT:                                                                                  \
-    return Zh ? gram_fused_nt<NT, true>(m, mr, A, lda, Zp, Zc, Zh, P, g_out, s)              \
-              : gram_fused_nt<NT, false>(m, mr, A, lda, Zp, Zc, nullptr, P, g_out, s);
+    return Zh ? gram_fused_nt<NT, true>(m, mr, A, lda, Zp, Zc, Zh, P, g_out, s, accum)       \
+              : gram_fused_nt<NT, false>(m, mr, A, lda, Zp, Zc, nullptr, P, g_out, s, accum);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

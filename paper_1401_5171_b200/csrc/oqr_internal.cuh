@@ -49,15 +49,17 @@ void timing_end(cudaStream_t s);
 cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s,
                           double scale = 1.0);
 // Per-CTA partial Gram slots P[g][NP][NP] of Z^T (A Z); returns the grid size used in *g_out.
-// A is moved by 2-D tensor TMA when it is 16-byte aligned with an even lda; otherwise by plain
-// loads (same results, slow).
+// A is moved by tensor TMA when it is 16-byte aligned with an even lda; otherwise by plain
+// loads (same results, slow).  accum: add to the slots instead of overwriting them (a later
+// column chunk of A; the grid must not exceed the first chunk's).
 // Rows [0, mr) of A (or of a row block of A holding mr rows, all m columns): slots of
 // Z_rows^T (A_rows Z) where Zp packs all m rows of Z (B operand) and Zc packs the mr rows of Z
 // that match the A rows (contraction operand; Zc == Zp on one GPU).  Zh != nullptr selects the
 // symmetric schedule (NEXT-N4; mr == m): only the block-lower triangle of A is read, Zh = Z/2
 // packed, and the slots hold T with G = T + T^T (launch_gram_reduce(..., sym = true)).
 cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int64_t lda, const double* Zp,
-                              const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s);
+                              const double* Zc, const double* Zh, double* P, int* g_out, cudaStream_t s,
+                              bool accum = false);
 // G (n x n, ldg) = sum_{c<count} P_c, P_c = n x n (ld n) consecutive, c ascending.
 cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s);
 // Zp and W = T Z (T = tridiag(e, d, e)), both packed, in one pass over Z.

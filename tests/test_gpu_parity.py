@@ -218,7 +218,12 @@ def cholqr_orth_bound(p, Qo, Ro):
 
 def variant_gates(oqr, p, variant, family="dense"):
     m, n = p.m, p.n
-    fams = {"dense": oqr.VARIANTS, "sym": oqr.VARIANTS_SYM}
+    fams = {"dense": oqr.VARIANTS, "sym": oqr.VARIANTS_SYM,
+            # oqr_normal_host: host arrays in and out, A staged in 64- or 128-column chunks
+            "host64": {"normal": lambda A, Z: oqr.normal_host(A.cpu(), Z.cpu(), chunk_cols=64)},
+            "host128": {"normal": lambda A, Z: oqr.normal_host(A.cpu().pin_memory(), Z.cpu().pin_memory(),
+                                                               chunk_cols=128)},
+            "host": {"normal": lambda A, Z: oqr.normal_host(A.cpu().pin_memory(), Z.cpu())}}
     Q, R, st = fams[family][variant](to_dev(p.A), to_dev(p.Z))
     Qo, Ro, sto = oracle.VARIANTS[variant](p.A, p.Z, m)
     cls = lambda s: 0 if s == 0 else (1 if s <= n else 2)
@@ -447,3 +452,42 @@ def test_tiny_shapes(oqr, variant, mn):
     Zd = np.abs(oracle.from_cm(p.Z, m))
     M = Zd.T @ (np.abs(oracle.from_cm(p.A, m)) @ Zd)
     assert np.all(np.abs(Gs - Go) <= 2 * gamma(3 * m) * M)
+
+
+# oqr_normal_host: the same CHOLQR on host arrays, A moved in column chunks with the Gram of each
+# chunk accumulated into the same slots (include/oqr.h).  Gates T2/T5/T6/T7 against the oracle
+# for several chunk sizes (64: a chunk per k-block group, ragged last chunk; auto = m/8), T8.
+@pytest.mark.parametrize("family", ["host64", "host128", "host"])
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"m{s[0]}n{s[1]}")
+def test_normal_host(oqr, shape, family):
+    variant_gates(oqr, make(*shape), "normal", family)
+
+
+def test_normal_host_determinism_and_gram(oqr):
+    p = make(4000, 50, 1e4, 1e3, 99, 3, 1)
+    Ah, Zh = torch.from_numpy(p.A).pin_memory(), torch.from_numpy(p.Z)
+    Q1, R1, s1 = oqr.normal_host(Ah, Zh, chunk_cols=192)
+    Q2, R2, s2 = oqr.normal_host(Ah, Zh, chunk_cols=192)
+    assert s1 == s2 == 0 and torch.equal(Q1, Q2) and torch.equal(R1, R2)                     # T8
+    # T3 on the chunked Gram: R^T R reproduces the oracle's G within eq.mult1-2 + eq:normal:chol
+    m, n = p.m, p.n
+    Go = oracle.from_cm(oracle.gram(p.A, p.Z, m), n)
+    Rd = R1.numpy().T
+    Ad, Zd = np.abs(oracle.from_cm(p.A, m)), np.abs(oracle.from_cm(p.Z, m))
+    M = Zd.T @ (Ad @ Zd)
+    assert np.all(np.abs(Rd.T @ Rd - Go) <= 2 * gamma(3 * m) * M + 2 * gamma(n + 1) * (np.abs(Rd).T @ np.abs(Rd)))
+
+
+def test_normal_host_argument_errors(oqr):
+    import ctypes
+    L = oqr.lib()
+    A = torch.zeros((64, 64), dtype=torch.float64)
+    Z = torch.zeros((8, 64), dtype=torch.float64)
+    Q = torch.zeros((8, 64), dtype=torch.float64)
+    R = torch.zeros((8, 8), dtype=torch.float64)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.oqr_normal_host(64, 8, None, 64, P(Z), 64, P(Q), P(R), 0, s) == -3
+    assert L.oqr_normal_host(64, 8, P(A), 63, P(Z), 64, P(Q), P(R), 0, s) == -4
+    assert L.oqr_normal_host(64, 8, P(A), 64, P(Z), 64, P(Q), P(R), -1, s) == -9
+    assert L.oqr_normal_host(64, 65, P(A), 64, P(Z), 64, P(Q), P(R), 0, s) == -2
