@@ -236,10 +236,28 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
   const bool has_entry = ctid < NCH * LG * 64;
   const int vch = ctid / (LG * 64), vj = (ctid >> 6) % LG, v64 = ctid & 63;
   const int vt = v64 >> 1, ve = v64 & 1;
+  // this thread's slot entry of chunk (kt, lg): p_lg + 8 kt.  Its previous value and the next
+  // tile-row's Z fragments are loaded one kt ahead (L2 latency off the per-chunk critical path).
+  double* pbase = slot + (int64_t)(2 * (vt & 3) + ve) * NP + (vt >> 2);
+  double pc[NG], pn[NG];
+#pragma unroll
+  for (int lg = 0; lg < NG; ++lg) {
+    const int tl = lg * LG + vj, lt = vch * NTW + tl;
+    const bool valid = has_entry && tl < NTW && lt < NT;
+    pc[lg] = (!first && valid) ? pbase[(int64_t)lt * 8 * NP] : 0.0;
+  }
+  double za0 = z0[0], za1 = z1[0];
 #pragma unroll 1
   for (int kt = 0; kt < NT; ++kt) {
-    const double za0 = z0[kt * 4 * FRAG];
-    const double za1 = z1[kt * 4 * FRAG];
+    const bool more = kt + 1 < NT;
+    const double zn0 = more ? z0[(kt + 1) * 4 * FRAG] : 0.0;
+    const double zn1 = more ? z1[(kt + 1) * 4 * FRAG] : 0.0;
+#pragma unroll
+    for (int lg = 0; lg < NG; ++lg) {
+      const int tl = lg * LG + vj, lt = vch * NTW + tl;
+      const bool valid = has_entry && tl < NTW && lt < NT;
+      pn[lg] = (!first && valid && more) ? pbase[(int64_t)lt * 8 * NP + (kt + 1) * 8] : 0.0;
+    }
 #pragma unroll
     for (int lg = 0; lg < NG; ++lg) {
 #pragma unroll
@@ -256,18 +274,20 @@ __device__ __forceinline__ void contract_panel(double (&acc)[(NT + 1) / 2][2], i
       const int tl = lg * LG + vj;
       const int lt = vch * NTW + tl;
       const bool valid = has_entry && tl < NTW && lt < NT;
-      double* p = slot + (int64_t)(lt * 8 + 2 * (vt & 3) + ve) * NP + kt * 8 + (vt >> 2);
-      const double prev = (!first && valid) ? *p : 0.0;  // L2 latency overlaps the barrier
       __syncthreads();
       if (valid) {
         const double* rr = red + (vch * NRG * LG + vj) * 64 + v64;
         double s = rr[0];
 #pragma unroll
         for (int g = 1; g < NRG; ++g) s += rr[g * LG * 64];
-        *p = first ? s : (prev + s);
+        pbase[(int64_t)lt * 8 * NP + kt * 8] = first ? s : (pc[lg] + s);
       }
       __syncthreads();
     }
+#pragma unroll
+    for (int lg = 0; lg < NG; ++lg) pc[lg] = pn[lg];
+    za0 = zn0;
+    za1 = zn1;
   }
 }
 

@@ -66,13 +66,18 @@ def sampled_cols(n):
     return sorted(set([0, 1, 2, 3, n // 2, n - 3, n - 2, n - 1]))[:SAMPLE_COLS]
 
 
-@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_stable", "normal_sym", "prequr_sym"])
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_stable", "normal_sym", "prequr_sym",
+                                     "normal_host"])
 def test_variants_full(case, variant):
     p, oqr = case["p"], case["oqr"]
     m, n = p.m, p.n
     if variant.endswith("_sym"):      # NEXT-N4: same mathematics, block-lower triangle of A only
         variant = variant[:-4]
         fn = oqr.VARIANTS_SYM[variant]
+    elif variant == "normal_host":    # host arrays in and out, A staged in column chunks
+        variant = "normal"
+        Ah, Zh = torch.from_numpy(p.A), torch.from_numpy(p.Z)
+        fn = lambda A, Z: oqr.normal_host(Ah, Zh)
     else:
         fn = oqr.VARIANTS[variant]
     Q, R, st = fn(case["A"], case["Z"])
