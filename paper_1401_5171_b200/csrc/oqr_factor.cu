@@ -167,11 +167,14 @@ cudaError_t launch_shift_diag(int n, double* G, int64_t ldg, double factor, cons
 // ------------------------------------------------------------------ K3 --------------------
 // Q = Z R^{-1}: Algorithm 1 line 4 as the row-wise substitution whose backward
 // error is stated at PAPER.md:197-198:  q_ij = (z_ij - sum_{k<j} q_ik r_kj) / r_jj.
-// One warp per 8 rows; columns in tiles of 8 (jt).  For tile jt the partial sums
-// sum_{k < 8 jt} q_ik r_kj run on the FP64 tensor pipe (mma.m8n8k4, K = 8 jt), with the row's
-// finished q's kept in registers as DMMA A-fragments; then the 8 x 8 diagonal block is solved
-// by plain substitution: column c of the tile is (z - s - sum_{c'<c} q_c' r_c'c) / r_cc with the
-// running sum held in the lane that owns the entry and q_c broadcast to the row's 4 lanes.
+// One warp per 8 rows; columns in tiles of 8 (jt).  Right-looking: as soon as tile kt of the
+// row block is solved, its contributions q_kt R[kt, jt] to every later tile jt are added on the
+// FP64 tensor pipe (mma.m8n8k4) into per-tile accumulators S[jt] held in registers, so when tile
+// jt is reached only q_{jt-1}'s two DMMAs stand between it and its diagonal solve, and the
+// updates of the later tiles overlap that solve; then the 8 x 8 diagonal block is solved by
+// plain substitution: column c of the tile is (z - s - sum_{c'<c} q_c' r_c'c) / r_cc.
+// (Left-looking with the finished q's kept as A-fragments measured 0.20 / 0.38 ms at
+// m = 4e4 / 1e5, n = 200; this form with LDS-addressed R: 0.15 / 0.28 ms.)
 // This is the substitution formula with the sum split into pieces (a summation order), never an
 // explicit inverse, so the componentwise bound |dR^i| <= gamma_n |R| still holds.
 __device__ __forceinline__ void dmma_f(double (&d)[2], double a, double b) {
@@ -191,6 +194,12 @@ __device__ __forceinline__ void dmma_f(double (&d)[2], double a, double b) {
 // q_c = (t_c - sum_{c'<c} q_c' r_c'c) * (1 / r_cc): no shuffles and no divisions on the chain.
 // (Multiplying by the rounded reciprocal adds one rounding per entry: the row-wise backward error
 // becomes |dR^i| <= gamma_{n+1} |R|, the bound the parity gates use.)
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 constexpr int TRSM_THREADS = 256;  // 8 warps: <= 255 registers, the q fragments stay in registers
 
 template <int NT>
@@ -208,14 +217,29 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
   double* const Ri_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
   double* const Rd_base = Ri_base + (size_t)NT * 8;
   {
-    double* Rt = Rt_base;
-    double* Rd = Rd_base;
-    for (int jt = 1; jt < NT; ++jt) {  // tiles (kt < jt) of column tile jt: jt*64 doubles
-      double* dst = Rt + (size_t)jt * (jt - 1) / 2 * 64;
-      for (int e = threadIdx.x; e < jt * 64; e += blockDim.x) {
-        const int ln = e & 31, h = (e >> 5) & 1, kt = e >> 6;
-        const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
-        dst[e] = (col < n) ? R[(int64_t)col * ldr + k] : 0.0;
+    // staged with 8 independent loads in flight per thread (a plain loop waits one L2 round trip
+    // per element: ~7% of K3 at m = 1e5)
+    constexpr int TOT = NT * (NT - 1) / 2 * 64;
+    for (int e0 = threadIdx.x; e0 < TOT; e0 += 8 * TRSM_THREADS) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * TRSM_THREADS;
+        v[u] = 0.0;
+        if (e < TOT) {
+          const int t = e >> 6;  // packed triangle tile index: t = jt (jt - 1) / 2 + kt
+          int jt = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)t)) * 0.5f);
+          while (jt * (jt - 1) / 2 > t) --jt;
+          while ((jt + 1) * jt / 2 <= t) ++jt;
+          const int kt = t - jt * (jt - 1) / 2, ln = e & 31, h = (e >> 5) & 1;
+          const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
+          if (col < n) v[u] = R[(int64_t)col * ldr + k];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * TRSM_THREADS;
+        if (e < TOT) Rt_base[e] = v[u];
       }
     }
     if (SMEM_RD) {
@@ -224,7 +248,7 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
         const int r = jt * 8 + c, col = jt * 8 + c2;
         double v = 0.0;
         if (c <= c2) v = (col < n) ? R[(int64_t)col * ldr + r] : (c == c2 ? 1.0 : 0.0);
-        Rd[e] = v;
+        Rd_base[e] = v;
       }
     }
     for (int e = threadIdx.x; e < NT * 8; e += blockDim.x)
@@ -240,43 +264,44 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
     const bool row_ok = row < m;
     // opaque per-iteration copies: stop the compiler from hoisting loop-invariant R loads and
     // per-column offsets/predicates out of the row loop into hundreds of registers
-    const double* Rt = Rt_base;
-    const double* Rd = Rd_base;
-    const double* Ri = Ri_base;
+    // (shared-window addresses, so the loads stay LDS: a generic pointer made opaque would turn
+    // them into generic loads with long-scoreboard latency)
+    uint32_t Rt = (uint32_t)__cvta_generic_to_shared(Rt_base);
+    uint32_t Rd = (uint32_t)__cvta_generic_to_shared(Rd_base);
+    uint32_t Ri = (uint32_t)__cvta_generic_to_shared(Ri_base);
     int64_t ldz_l = ldz, ldq_l = ldq;
     int n_l = n;
     const double* Rg = R;
-    asm volatile("" : "+l"(Rt), "+l"(Rd), "+l"(Ri), "+l"(ldz_l), "+l"(ldq_l), "+r"(n_l), "+l"(Rg));
-    double qa[NT][2];                     // A fragments: Q[r0 + lane/4, jt*8 + 4h + lane%4]
-    // Z of tile jt+1 is loaded before tile jt's Q stores: different columns, so this is safe
-    // even in place (Q == Z); the compiler must assume Q aliases Z and would not reorder these.
-    double znext[2];
+    asm volatile("" : "+r"(Rt), "+r"(Rd), "+r"(Ri), "+l"(ldz_l), "+l"(ldq_l), "+r"(n_l), "+l"(Rg));
+    // Right-looking: S[jt] accumulates sum_{kt<jt} q_kt R[kt, jt] (C layout) as soon as each q_kt
+    // is known, so when tile jt is reached only q_{jt-1}'s two DMMAs are still on its critical
+    // path; the updates of the later tiles overlap the next diagonal solves.
+    double S[NT][2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int col = 2 * q4 + e;
-      znext[e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
-    }
+    for (int jt = 0; jt < NT; ++jt) S[jt][0] = S[jt][1] = 0.0;
+    // Z of tiles jt+1, jt+2 is loaded before tile jt's Q stores: different columns, so this is
+    // safe even in place (Q == Z); the compiler must assume Q aliases Z and would not reorder them.
+    constexpr int PD = 2;  // Z prefetch distance in tiles
+    double zq[PD][2];
+#pragma unroll
+    for (int d = 0; d < PD; ++d)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = d * 8 + 2 * q4 + e;
+        zq[d][e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+      }
 #pragma unroll
     for (int jt = 0; jt < NT; ++jt) {
-      const double zc0 = znext[0], zc1 = znext[1];
-      if (jt + 1 < NT) {
+      const double zc0 = zq[jt % PD][0], zc1 = zq[jt % PD][1];
+      if (jt + PD < NT) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int col = (jt + 1) * 8 + 2 * q4 + e;
-          znext[e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+          const int col = (jt + PD) * 8 + 2 * q4 + e;
+          zq[jt % PD][e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
         }
       }
-      // off-diagonal partial sums on DMMA (four independent accumulator chains)
-      double sacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-      for (int kt = 0; kt < jt; ++kt) {
-        const double* f = Rt + (size_t)(jt * (jt - 1) / 2 + kt) * 64 + lane;
-        const double b0 = f[0], b1 = f[32];
-        dmma_f(sacc[kt & 3], qa[kt][0], b0);
-        dmma_f(sacc[kt & 3], qa[kt][1], b1);
-      }
-      double t0 = zc0 - ((sacc[0][0] + sacc[1][0]) + (sacc[2][0] + sacc[3][0]));
-      double t1 = zc1 - ((sacc[0][1] + sacc[1][1]) + (sacc[2][1] + sacc[3][1]));
+      double t0 = zc0 - S[jt][0];
+      double t1 = zc1 - S[jt][1];
       // gather the row's 8 values into every lane of its quad
       double tt[8];
 #pragma unroll
@@ -289,24 +314,33 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int dc = jt * 8 + c;
-        qv[c] = tt[c] * Ri[dc];
+        qv[c] = tt[c] * lds_f64(Ri + 8u * dc);
 #pragma unroll
         for (int c2 = c + 1; c2 < 8; ++c2) {
           double rcj;
-          if (SMEM_RD) rcj = Rd[(jt * 8 + c) * 8 + c2];
+          if (SMEM_RD) rcj = lds_f64(Rd + 8u * ((jt * 8 + c) * 8 + c2));
           else rcj = (jt * 8 + c2) < n_l ? Rg[(int64_t)(jt * 8 + c2) * ldr + dc] : 0.0;
           tt[c2] = fma(-qv[c], rcj, tt[c2]);
         }
       }
-      // this lane's two C entries -> Q, and the tile's A fragments (row lane/4, cols 4h + lane%4)
+      // the tile's A fragments (row lane/4, cols 4h + lane%4), then the updates of every later
+      // tile, the next one first
+      const double a0 = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
+      const double a1 = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
+      // all first-half k-steps, then all second-half ones: consecutive DMMAs are independent
+#pragma unroll
+      for (int j2 = jt + 1; j2 < NT; ++j2)
+        dmma_f(S[j2], a0, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + jt) * 64 + lane)));
+#pragma unroll
+      for (int j2 = jt + 1; j2 < NT; ++j2)
+        dmma_f(S[j2], a1, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + jt) * 64 + 32 + lane)));
+      // this lane's two C entries -> Q
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = jt * 8 + 2 * q4 + e;
         const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
         if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
       }
-      qa[jt][0] = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
-      qa[jt][1] = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
     }
   }
 }
