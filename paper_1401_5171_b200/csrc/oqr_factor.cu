@@ -33,9 +33,27 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
   if (!first && *info != 0) return;  // an earlier stage already broke down: keep its code
   const int NT = (n + 7) / 8, NP = NT * 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-  for (int l = warp; l < NP; l += nwarp)
-    for (int k = lane; k <= l; k += 32)
-      S[pk(k, l)] = (l < n) ? G[(int64_t)l * ldg + k] : (k == l ? 1.0 : 0.0);
+  {  // packed upper triangle of G, padded with an identity block; 8 loads in flight per thread
+    const int tot = NP * (NP + 1) / 2;
+    for (int e0 = tid; e0 < tot; e0 += 8 * 1024) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 1024;
+        v[u] = 0.0;
+        if (e < tot) {
+          int l = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+          while (l * (l + 1) / 2 > e) --l;
+          while ((l + 1) * (l + 2) / 2 <= e) ++l;
+          const int k = e - l * (l + 1) / 2;
+          v[u] = (l < n) ? G[(int64_t)l * ldg + k] : (k == l ? 1.0 : 0.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * 1024 < tot) S[e0 + u * 1024] = v[u];
+    }
+  }
   if (tid == 0) s_brk = 0;
   __syncthreads();
   __shared__ double s_inv[2][8];  // reciprocals of the diagonal blocks' pivots (double-buffered)
@@ -44,31 +62,54 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
   auto factor_diag = [&](int jb) {
     const int b0 = jb * 8;
     double* inv_out = s_inv[jb & 1];
+#ifdef OQR_EXP_POTRF_NOFACTOR  // experiment build only: time of everything but the diagonal factor
+    if (lane < 8) inv_out[lane] = 1.0;
+    __syncwarp();
+    return;
+#endif
+    // The 8 x 8 block in registers: lane L holds entries (L/8, L%8) and (L/8 + 4, L%8) (upper
+    // part meaningful); pivots and scaled rows travel by shuffles -- the same operations, in the
+    // same order, as the unblocked LAPACK loop on the block.
+    const int ra = lane >> 3, cb = lane & 7;
+    double v0 = (cb >= ra) ? S[pk(b0 + ra, b0 + cb)] : 0.0;
+    double v1 = (cb >= ra + 4) ? S[pk(b0 + ra + 4, b0 + cb)] : 0.0;
+    int brk = 0;
+#pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const int p = b0 + c;
-      const double d = S[pk(p, p)];
+      // pivot (c, c): lane 9c (c < 4, v0) or 9c - 32 (c >= 4, v1)
+      const double d = __shfl_sync(0xffffffffu, c < 4 ? v0 : v1, c < 4 ? 9 * c : 9 * c - 32);
       if (!(d > 0.0)) {  // uniform across the warp
-        if (lane == 0) s_brk = p + 1;
+        brk = b0 + c + 1;
         break;
       }
       const double r = sqrt(d);
       const double inv = 1.0 / r;
-      __syncwarp();
-      if (lane < 7 - c) S[pk(p, p + 1 + lane)] *= inv;
-      if (lane == 0) {
-        S[pk(p, p)] = r;
-        inv_out[c] = inv;
+      // row c: (c, c) = r, (c, b > c) *= inv
+      if (c < 4) {
+        if (ra == c) v0 = (cb == c) ? r : (cb > c ? v0 * inv : v0);
+      } else {
+        if (ra + 4 == c) v1 = (cb == c) ? r : (cb > c ? v1 * inv : v1);
       }
-      __syncwarp();
-      for (int e = lane; e < 64; e += 32) {
-        const int a = e >> 3, b = e & 7;
-        if (a > c && b >= a) S[pk(b0 + a, b0 + b)] -= S[pk(p, b0 + a)] * S[pk(p, b0 + b)];
-      }
-      __syncwarp();
+      if (lane == 0) inv_out[c] = inv;
+      // trailing: (a, b) -= r_ca r_cb for c < a <= b; r_cx lives in lane c*8 + x (mod 32)
+      const double rc0 = c < 4 ? v0 : v1;
+      const int src = (c & 3) * 8;
+      const double ra0 = __shfl_sync(0xffffffffu, rc0, src + ra);        // r_{c, ra}
+      const double ra1 = __shfl_sync(0xffffffffu, rc0, src + ((ra + 4) & 7));  // r_{c, ra+4}
+      const double rb = __shfl_sync(0xffffffffu, rc0, src + cb);         // r_{c, cb}
+      if (ra > c && cb >= ra) v0 -= ra0 * rb;
+      if (ra + 4 > c && cb >= ra + 4) v1 -= ra1 * rb;
     }
+    if (cb >= ra) S[pk(b0 + ra, b0 + cb)] = v0;
+    if (cb >= ra + 4) S[pk(b0 + ra + 4, b0 + cb)] = v1;
+    if (brk && lane == 0) s_brk = brk;
+    __syncwarp();
   };
   // one 8x8 tile of the trailing update: A_{k0.., l0..} -= R_{j0.., k0..}^T R_{j0.., l0..}
   auto update_tile = [&](int j0, int k0, int l0) {
+#ifdef OQR_EXP_POTRF_NOTRAIL  // experiment build only: no trailing update
+    return;
+#endif
     double acc[2] = {0.0, 0.0};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
