@@ -20,6 +20,10 @@ for _ in range(reps):
     oqr.potrf(G, R, info)
 e1.record()
 torch.cuda.synchronize()
-ok = torch.allclose(R @ R.T, G, rtol=1e-10, atol=1e-8 * float(G.abs().max()))
+# oqr.potrf stores R column-major: the (n, n) tensor holds R^T row-wise
+Rm = R.T.cpu()
+Rref = torch.linalg.cholesky(G.cpu()).T
+ok = bool(torch.allclose(Rm, Rref, rtol=1e-12, atol=1e-12 * float(Rref.abs().max()))) and \
+    bool(torch.equal(torch.tril(Rm, -1), torch.zeros_like(Rm)))
 print(f"{os.path.basename(oqr.LIB_PATH)} potrf n={n}: {e0.elapsed_time(e1) / reps * 1e3:.1f} us  info={int(info.item())}  "
       f"R^T R == G: {ok}")
