@@ -18,6 +18,9 @@ roofline = the fused Gram kernel K1, timed live with CUDA events on the launchin
 cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample: the leading r x r
            principal block of the same A and the first r rows of Z.
 --impl reference: the oracle itself timed as the reference arm (rank 0 only).
+--sym: the NEXT-N4 symmetric family (block-lower triangle of A; own roofline).
+--tridiag: the NEXT-N3 second workload (tridiagonal A, m = 100000, n = 200; paper normalisation
+           2mn^2; roofline on the packed Gram K4').
 """
 from __future__ import annotations
 
@@ -166,6 +169,105 @@ def reference_arm(args, cfg, rank):
     print(json.dumps(line), flush=True)
 
 
+def bench_tridiag(args):
+    """The paper's second workload (fig.perf-tridiag): A = tridiag(e, d, e),
+    m = 100000, n = 200 (gen.TRIDIAG_CONFIGS["T"]), flops normalised 2 m n^2.  Roofline on the
+    packed Gram K4' (G = Z^T (T Z) on DMMA, 2 m n^2 flops per launch), timed live by the hook."""
+    import torch
+    import oracle
+    import paper_1401_5171_b200 as oqr
+    d, e, p = gen.tridiag_config("T")
+    m, n = p.m, p.n
+    fl = 2.0 * m * n * n
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    d_h, e_h, Z_h = torch.from_numpy(d).pin_memory(), torch.from_numpy(e).pin_memory(), torch.from_numpy(p.Z)
+    Z_h = Z_h.pin_memory()
+    dg, eg, Z = d_h.to(dev), e_h.to(dev), Z_h.to(dev)
+    Q = torch.empty((n, m), dtype=torch.float64, device=dev)
+    R = torch.empty((n, n), dtype=torch.float64, device=dev)
+    Q_h = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+    R_h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    fn = oqr.VARIANTS_TRIDIAG[args.variant]
+    for _ in range(args.warmup):
+        assert fn(dg, eg, Z, Q, R)[2] == 0
+    oqr.timing_enable(True)
+    oqr.timing_reset()
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sts = [fn(dg, eg, Z, Q, R)[2] for _ in range(args.steps)]
+        e1.record(stream)
+        torch.cuda.synchronize()
+    assert all(st == 0 for st in sts), sts
+    ms_step = e0.elapsed_time(e1) / args.steps
+    kern = {k: oqr.timing_read_kernel(k) for k in ("K4", "K3", "K2")}
+    _, _, launches = oqr.timing_read()
+    oqr.timing_enable(False)
+    k4_ms = kern["K4"][0] / max(kern["K4"][1], 1)
+    NP = 8 * ((n + 7) // 8)
+    fl_k4 = 2.0 * m * NP * NP
+    achieved = fl_k4 / (k4_ms * 1e-3) / 1e12
+    # e2e: d, e, Z in from pinned host memory, Q, R out, every step
+    h2d = (d_h.numel() + e_h.numel() + Z_h.numel()) * 8
+    d2h = (Q_h.numel() + R_h.numel()) * 8
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        dg.copy_(d_h, non_blocking=True)
+        eg.copy_(e_h, non_blocking=True)
+        Z.copy_(Z_h, non_blocking=True)
+        Qs, Rs, st = fn(dg, eg, Z, Q, R)
+        Q_h.copy_(Qs, non_blocking=True)
+        R_h.copy_(Rs, non_blocking=True)
+        assert st == 0
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_value = fl / (e0.elapsed_time(e1) / args.e2e_steps * 1e-3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:   # the oracle on the leading mc rows (a tridiagonal of size mc)
+        threads = len(os.sched_getaffinity(0))
+        mc = m          # the whole problem takes well under a second on the host
+        Zc = np.ascontiguousarray(p.Z[:, :mc])
+        t = time.perf_counter()
+        _, _, sto = oracle.VARIANTS_TRIDIAG[args.variant](d[:mc], e[:mc - 1], Zc, mc)
+        dt = time.perf_counter() - t
+        cpu = {"value": 2.0 * mc * n * n / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+               "sample": f"oracle {args.variant}_tridiag on the leading {mc} rows (tridiagonal of size {mc}, "
+                         f"n={n}); {dt:.1f} s; OMP threads={threads}"}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k4_tridiag_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    line = {
+        "metric": "oblique-QR GFLOP/s, tridiagonal A (FP64, 1 B200; paper normalisation 2mn^2)",
+        "value": fl / (ms_step * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"tridiag T oqr_{args.variant}_tridiag: m={m}, n={n}, kappa_A=1e3, kappa_Z=1e2",
+                   "m": m, "n": n, "variant": args.variant, "flops_per_step": fl,
+                   "flop_normalisation": "2mn^2 (PAPER.md:960-961)",
+                   "l2": "Z = %.0f MB, packed Z and T Z = %.0f MB > L2; no flush" % (8e-6 * m * n, 16e-6 * m * NP)},
+        "roofline": {"bound": "tensor", "kernel": "gram_packed (K4'): G = Z^T (T Z)", "achieved": achieved,
+                     "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+                     "traffic": traffic, "algorithmic_flops_per_launch": fl_k4, "mean_launch_ms": k4_ms,
+                     "share_of_step": k4_ms / ms_step, "peak_source": PEAK_SOURCE,
+                     "other_kernels_ms": {"trsm (K3)": kern["K3"][0] / max(kern["K3"][1], 1),
+                                          "potrf (K2)": kern["K2"][0] / max(kern["K2"][1], 1)}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": args.e2e_steps, "api": f"H2D copies + oqr_{args.variant}_tridiag + D2H copies"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 _registered = []
 
 
@@ -195,6 +297,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sym", action="store_true",
                     help="NEXT-N4 symmetric family: block-lower triangle of A only (own roofline)")
+    ap.add_argument("--tridiag", action="store_true",
+                    help="NEXT-N3 second workload: A tridiagonal, m = 100000, n = 200 (paper's 2mn^2 "
+                         "normalisation, own roofline on the packed Gram K4')")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded code path even at N = 1 (it is the default for N > 1)")
     args = ap.parse_args()
@@ -206,6 +311,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         reference_arm(args, args.config, rank)
+        return
+    if args.tridiag:
+        assert world == 1, "--tridiag is a single-GPU workload"
+        bench_tridiag(args)
         return
 
     import torch

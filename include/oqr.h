@@ -235,6 +235,14 @@ int oqr_sum_partials(int64_t n, int64_t count, const double* P, double* G, oqr_s
 void oqr_timing_enable(int enable);
 void oqr_timing_reset(void);
 int oqr_timing_read(double* gram_ms, int64_t* gram_launches, int64_t* total_launches);
+/* The same hook for one kernel family: OQR_TIMING_K1 (fused Gram, as oqr_timing_read),
+ * OQR_TIMING_K4 (packed tall-skinny Gram: Euclidean / tridiagonal), OQR_TIMING_K3 (triangular
+ * solve), OQR_TIMING_K2 (Cholesky).  Status 0, -1 unknown kernel, -100 CUDA. */
+#define OQR_TIMING_K1 0
+#define OQR_TIMING_K4 1
+#define OQR_TIMING_K3 2
+#define OQR_TIMING_K2 3
+int oqr_timing_read_kernel(int kernel, double* ms, int64_t* launches);
 
 /* Number of kernels this library has launched since load (all entry points). */
 int64_t oqr_launch_count(void);

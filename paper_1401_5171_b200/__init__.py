@@ -30,7 +30,8 @@ EXPORTS = ("oqr_normal", "oqr_normal_host", "oqr_normal2", "oqr_prequr", "oqr_wo
            "oqr_gram_sym", "oqr_upload_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
            "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_gram_rows", "oqr_sum_partials",
-           "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_launch_count")
+           "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_timing_read_kernel",
+           "oqr_launch_count")
 
 
 class OqrError(RuntimeError):
@@ -95,6 +96,8 @@ def lib() -> ctypes.CDLL:
         L.oqr_timing_read.restype = I
         L.oqr_timing_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64),
                                       ctypes.POINTER(I64)]
+        L.oqr_timing_read_kernel.restype = I
+        L.oqr_timing_read_kernel.argtypes = [I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
         L.oqr_launch_count.restype = I64
         L.oqr_launch_count.argtypes = []
         _lib = L
@@ -443,6 +446,20 @@ def timing_enable(on: bool = True):
 
 def timing_reset():
     lib().oqr_timing_reset()
+
+
+TIMING_KERNELS = {"K1": 0, "K4": 1, "K3": 2, "K2": 3}
+
+
+def timing_read_kernel(kernel: str) -> tuple[float, int]:
+    """(accumulated milliseconds, launches) of one kernel family ("K1" fused Gram, "K4" packed
+    Gram, "K3" triangular solve, "K2" Cholesky) since the last timing_reset."""
+    ms = ctypes.c_double()
+    k = ctypes.c_int64()
+    st = lib().oqr_timing_read_kernel(TIMING_KERNELS[kernel], ctypes.byref(ms), ctypes.byref(k))
+    if st:
+        raise OqrError(st, "oqr_timing_read_kernel")
+    return ms.value, k.value
 
 
 def timing_read() -> tuple[float, int, int]:

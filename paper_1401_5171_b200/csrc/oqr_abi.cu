@@ -17,6 +17,7 @@ namespace oqr {
 static std::atomic<int64_t> g_launches{0};
 static bool g_timing = false;
 static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+static std::vector<int> g_event_kind;  // TK_* of each used pair
 static size_t g_event_used = 0;
 static int64_t g_timing_total_launches0 = 0;
 
@@ -36,14 +37,16 @@ cudaError_t ensure_smem_attr(const void* func, int bytes) {
   return e;
 }
 
-void timing_begin(cudaStream_t s) {
+void timing_begin(cudaStream_t s, int kind) {
   if (!g_timing) return;
   if (g_event_used == g_events.size()) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     g_events.emplace_back(a, b);
+    g_event_kind.push_back(0);
   }
+  g_event_kind[g_event_used] = kind;
   cudaEventRecord(g_events[g_event_used].first, s);
 }
 
@@ -682,16 +685,26 @@ void oqr_timing_reset(void) {
   g_timing_total_launches0 = g_launches.load();
 }
 
-int oqr_timing_read(double* gram_ms, int64_t* gram_launches, int64_t* total_launches) {
+int oqr_timing_read_kernel(int kernel, double* ms_out, int64_t* launches) {
+  if (kernel < 0 || kernel > 3) return -1;
   double ms = 0.0;
+  int64_t k = 0;
   for (size_t i = 0; i < g_event_used; ++i) {
+    if (g_event_kind[i] != kernel) continue;
     if (cudaEventSynchronize(g_events[i].second) != cudaSuccess) return -100;
     float t = 0.f;
     if (cudaEventElapsedTime(&t, g_events[i].first, g_events[i].second) != cudaSuccess) return -100;
     ms += t;
+    ++k;
   }
-  if (gram_ms) *gram_ms = ms;
-  if (gram_launches) *gram_launches = (int64_t)g_event_used;
+  if (ms_out) *ms_out = ms;
+  if (launches) *launches = k;
+  return 0;
+}
+
+int oqr_timing_read(double* gram_ms, int64_t* gram_launches, int64_t* total_launches) {
+  const int st = oqr_timing_read_kernel(OQR_TIMING_K1, gram_ms, gram_launches);
+  if (st) return st;
   if (total_launches) *total_launches = g_launches.load() - g_timing_total_launches0;
   return 0;
 }

@@ -179,9 +179,12 @@ cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t
   const size_t bytes = (size_t)NP * (NP + 1) / 2 * sizeof(double);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(potrf_kernel), SMEM_MAX - 1024);
   if (e != cudaSuccess) return e;
+  timing_begin(s, OQR_TIMING_K2);
   potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off, first);
   note_launch();
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  timing_end(s);
+  return e;
 }
 
 // ------------------------------------------------------------------ shift -----------------
@@ -404,8 +407,11 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   int64_t g = cdiv(m, (TRSM_THREADS / 32) * 8);  // 8 rows per warp per pass
   const int sms = trsm_num_sms();
   if (g > sms) g = sms;          // persistent: R is staged once per CTA
+  timing_begin(s, OQR_TIMING_K3);
   trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, TRSM_THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
-  return cudaSuccess;
+  e = cudaGetLastError();
+  timing_end(s);
+  return e;
 }
 
 #define OQR_TRSM_CASES(X) \

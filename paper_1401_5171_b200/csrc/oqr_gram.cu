@@ -897,7 +897,7 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
   std::memset(&tmap, 0, sizeof(tmap));
   const int alay = (mr % 8) != 0 ? ALAY_COL : (NT == 1 ? ALAY_R8 : ALAY_R4);
   const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda, KS, alay);
-  timing_begin(s);
+  timing_begin(s, OQR_TIMING_K1);
   static const char* env_w = getenv("OQR_PANEL_W");
   // panel weight in units: a unit carries KS/16 times the work of a 16-wide unit
   const double panel_w = env_w ? atof(env_w) : PANEL_W_PER_NT * NT * (16.0 / KS);
@@ -926,9 +926,12 @@ static cudaError_t gram_packed_nt(int64_t m, const double* Xp, const double* Yp,
   int64_t nsl = num_sms() / NCP;
   if (nsl > nblk) nsl = nblk;
   *g_out = (int)nsl;
+  timing_begin(s, OQR_TIMING_K4);
   gram_packed_kernel<NT><<<dim3((unsigned)nsl, NCP), 256, bytes, s>>>(Xp, Yp, (int)nblk, P, stages);
   note_launch();
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  timing_end(s);
+  return e;
 }
 
 #define OQR_NT_CASES(X) \

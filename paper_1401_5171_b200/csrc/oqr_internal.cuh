@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/oqr.h"
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "liboqr is written for sm_100a (B200) only"
 #endif
@@ -41,7 +43,8 @@ inline int64_t zp_doubles(int64_t m, int NP) { return zp_blocks(m) * (NP / 8) * 
 void note_launch();
 // Raise a kernel's dynamic shared-memory limit once per (kernel, device) -- thread-safe.
 cudaError_t ensure_smem_attr(const void* func, int bytes);
-void timing_begin(cudaStream_t s);
+// kind: OQR_TIMING_K1 / _K4 / _K3 / _K2 (include/oqr.h)
+void timing_begin(cudaStream_t s, int kind);
 void timing_end(cudaStream_t s);
 
 // ---- launchers (return cudaError_t of the launch) ----
