@@ -107,7 +107,7 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
-def cpu_oracle_sample(p, target_s: float = 12.0):
+def cpu_oracle_sample(p, target_s: float = 12.0, lead=None):
     """Time the CPU oracle (as it stands) on the leading r x r principal block of the config's A
     and the first r rows of Z, with r sized for ~target_s of work.  Returns the cpu_baseline dict."""
     import oracle
@@ -115,7 +115,8 @@ def cpu_oracle_sample(p, target_s: float = 12.0):
     threads = len(os.sched_getaffinity(0))
 
     def run(r):
-        A = np.ascontiguousarray(p.A[:r, :r])
+        # the leading r x r principal block of A (lead(r) when this process holds only a row shard)
+        A = np.ascontiguousarray(lead(r) if p.A is None else p.A[:r, :r])
         Z = np.ascontiguousarray(p.Z[:, :r])
         t = time.perf_counter()
         _, _, st = oracle.normal(A, Z, r)
@@ -323,7 +324,7 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or (args.sharded and "RANK" in os.environ):  # torchrun: the NCCL exchange runs
         dist.init_process_group("nccl", device_id=dev)
     c = gen.CONFIGS[args.config]
     m, n = c["m"], c["n"]
@@ -444,7 +445,8 @@ def main():
                 pass
         cpu = None
         if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only
-            cpu, _, _ = cpu_oracle_sample(p)
+            cpu, _, _ = cpu_oracle_sample(
+                p, lead=lambda r: gen.config_A_rows(args.config, 0, r)[:r, :r])
         peaks = measured_peaks()
         line = {
             "metric": METRIC,
@@ -473,7 +475,7 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 

@@ -62,7 +62,7 @@ def normal_rows(Ar, Z, r0: int, mr: int, group=None, steps=None):
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     n = Z.shape[0]
     G_r = steps.gram_rows(Ar, Z, r0, mr)
-    if world > 1:
+    if dist.is_initialized():  # the exchange step runs whenever there is a group (also world = 1)
         gathered = torch.empty((world, n, n), dtype=G_r.dtype, device=G_r.device)
         if G_r.is_cuda and dist.get_backend(group) == "gloo":
             # gloo exchanges host tensors: stage the 8 n^2-byte partials through host memory

@@ -65,3 +65,29 @@ def test_normal_rows_world1_matches_normal(oqr):
     Q2, R2, s2 = oqr.normal(A, Z)
     assert s1 == s2 == 0
     assert torch.equal(R1, R2) and torch.equal(Q1, Q2)
+
+
+def test_normal_rows_over_a_one_rank_nccl_group(oqr):
+    """The exchange step of the row-sharded path (all-gather of the n x n partials in rank order,
+    then the fixed-order sum) through NCCL on this GPU: a one-rank group, so no rank waits on
+    another; with one shard the result is bitwise oqr_normal's."""
+    import socket
+    import torch.distributed as dist
+    from paper_1401_5171_b200.dist import normal_rows
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        p = gen.problem(1000, 40, 1e3, 1e2, 8)
+        A = torch.from_numpy(p.A).cuda()
+        Z = torch.from_numpy(p.Z).cuda()
+        Q1, R1, s1 = normal_rows(A, Z, 0, 1000)
+        Q2, R2, s2 = oqr.normal(A, Z)
+        assert s1 == s2 == 0
+        assert torch.equal(R1, R2) and torch.equal(Q1, Q2)
+    finally:
+        dist.destroy_process_group()
