@@ -71,7 +71,7 @@ res = {"gram (pack+K1+K1r)": timed(lambda: oqr.gram(A, Z, G)),
        "gram_euclid (pack+K4+K1r)": timed(lambda: oqr.gram_euclid(Z, m=m)),
        "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)),
        "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
-for v in ("normal", "normal2", "prequr"):
+for v in ("normal", "normal2", "prequr", "prequr_stable"):
     Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
     Rv = torch.empty((n, n), dtype=torch.float64, device="cuda")
     res[v] = timed(lambda: oqr.VARIANTS[v](A, Z, Q, Rv))
