@@ -84,3 +84,18 @@ def test_A_rows_bitwise_equal_to_full_rows():
     for r0, r1 in ((0, 64), (64, 200), (200, 333), (17, 18)):
         blk = gen.A_rows(333, 1e4, 19, r0, r1, lda=r1 - r0 + 2)
         assert np.array_equal(blk[:, : r1 - r0].T, full[r0:r1, :])
+
+
+def test_input_bytes_match_the_recorded_hashes():
+    """the bytes of the generated inputs are recorded (profiles/r01_input_hashes.txt,
+    tools/input_hashes.py); the small ones are regenerated here and must match bit for bit."""
+    import hashlib
+    import os
+    rec = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                            "r01_input_hashes.txt")).read().splitlines()
+    sha = lambda a: hashlib.sha256(memoryview(a).cast("B")).hexdigest()
+    for k in (0, 1):
+        p = gen.config(k)
+        assert f"configs[{k}] m={p.m} n={p.n}  A {sha(p.A)}  Z {sha(p.Z)}" in rec
+    d, e, p = gen.tridiag_config("t")
+    assert f"tridiag t m={p.m} n={p.n}  d {sha(d)}  e {sha(e)}  Z {sha(p.Z)}" in rec
