@@ -123,7 +123,11 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
     }
   };
   if (warp == 0) factor_diag(0);
+#ifdef OQR_EXP_POTRF_LOADSTORE  // experiment build only: launch + staging of G + write of R
+  for (int j = 0; j < 0; ++j) {
+#else
   for (int j = 0; j < NT; ++j) {
+#endif
     const int j0 = j * 8;
     __syncthreads();  // diagonal block j factored (look-ahead by warp 0)
     if (s_brk) break;
