@@ -248,7 +248,9 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
-constexpr int TRSM_THREADS = 256;  // 8 warps: <= 255 registers, the q fragments stay in registers
+// Warps per CTA: as many as the per-tile register accumulators allow without spills (ptxas:
+// 16 warps <= 128 registers up to NT = 16, 12 warps <= 168 up to NT = 29, else 8).
+__host__ __device__ constexpr int trsm_threads(int NT) { return NT <= 16 ? 512 : (NT <= 29 ? 384 : 256); }
 
 template <int NT>
 constexpr size_t trsm_smem_doubles(bool with_rd) {
@@ -256,7 +258,7 @@ constexpr size_t trsm_smem_doubles(bool with_rd) {
 }
 
 template <int NT, bool SMEM_RD>
-__global__ void __launch_bounds__(TRSM_THREADS, 1)
+__global__ void __launch_bounds__(trsm_threads(NT), 1)
 trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q (in place)
                  const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info) {
   if (info != nullptr && *info != 0) return;
@@ -268,11 +270,11 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
     // staged with 8 independent loads in flight per thread (a plain loop waits one L2 round trip
     // per element: ~7% of K3 at m = 1e5)
     constexpr int TOT = NT * (NT - 1) / 2 * 64;
-    for (int e0 = threadIdx.x; e0 < TOT; e0 += 8 * TRSM_THREADS) {
+    for (int e0 = threadIdx.x; e0 < TOT; e0 += 8 * trsm_threads(NT)) {
       double v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * TRSM_THREADS;
+        const int e = e0 + u * trsm_threads(NT);
         v[u] = 0.0;
         if (e < TOT) {
           const int t = e >> 6;  // packed triangle tile index: t = jt (jt - 1) / 2 + kt
@@ -286,7 +288,7 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * TRSM_THREADS;
+        const int e = e0 + u * trsm_threads(NT);
         if (e < TOT) Rt_base[e] = v[u];
       }
     }
@@ -408,11 +410,12 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   static_assert(bytes <= (size_t)SMEM_MAX, "R fragments must fit in shared memory");
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(trsm_dmma_kernel<NT, smem_rd>), (int)bytes);
   if (e != cudaSuccess) return e;
-  int64_t g = cdiv(m, (TRSM_THREADS / 32) * 8);  // 8 rows per warp per pass
+  constexpr int THREADS = trsm_threads(NT);
+  int64_t g = cdiv(m, (THREADS / 32) * 8);  // 8 rows per warp per pass
   const int sms = trsm_num_sms();
   if (g > sms) g = sms;          // persistent: R is staged once per CTA
   timing_begin(s, OQR_TIMING_K3);
-  trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, TRSM_THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
+  trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
   e = cudaGetLastError();
   timing_end(s);
   return e;
