@@ -641,8 +641,8 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
 // accumulators, so no cross-warp reduction is needed; the slot of the slice is written once.
 template <int NT>
 __device__ __forceinline__ void packed_issue(double* dst, const double* __restrict__ Xp, const double* __restrict__ Yp,
-                                            int bn, int hl0, int NTH, uint64_t* bar, uint64_t pol) {
-  const uint32_t xb = NT * 4 * FRAG * 8, yb = NTH * 4 * FRAG * 8;
+                                            int bn, int hl0, int NTH, uint64_t* bar, uint64_t pol, int NX = NT) {
+  const uint32_t xb = NX * 4 * FRAG * 8, yb = NTH * 4 * FRAG * 8;
   mbar_arrive_expect_tx(bar, xb + yb);
   bulk_g2s(dst, Xp + (int64_t)bn * NT * 4 * FRAG, xb, bar, pol);
   if (yb) bulk_g2s(dst + NT * 4 * FRAG, Yp + ((int64_t)bn * NT + hl0) * 4 * FRAG, yb, bar, pol);
@@ -654,7 +654,8 @@ template <int NT, int KT, int LT>
 __device__ __forceinline__ void packed_gram_body(double* ring, int STAGE, uint64_t* full, uint64_t* empty,
                                                  unsigned* relcnt, int stages, int b0, int b1, int kt0, int lt0,
                                                  int hl0, int NTH, const double* __restrict__ Xp,
-                                                 const double* __restrict__ Yp, double* slot, int lane, uint64_t pol) {
+                                                 const double* __restrict__ Yp, double* slot, int lane, uint64_t pol,
+                                                 int NX = NT) {
   constexpr int NP = NT * 8;
   double acc[KT > 0 ? KT : 1][LT > 0 ? LT : 1][2];
 #pragma unroll
@@ -688,7 +689,7 @@ __device__ __forceinline__ void packed_gram_body(double* ring, int STAGE, uint64
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last && b + stages < b1) {
       mbar_wait(&empty[s], ph);
-      if (lane == 0) packed_issue<NT>(ring + s * STAGE, Xp, Yp, b + stages, hl0, NTH, &full[s], pol);
+      if (lane == 0) packed_issue<NT>(ring + s * STAGE, Xp, Yp, b + stages, hl0, NTH, &full[s], pol, NX);
       __syncwarp();
     }
     if (++s == stages) {
@@ -758,16 +759,107 @@ gram_packed_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp,
                                            Xp, Yp, slot, lane, pol);
 }
 
+// K4' for a symmetric product (X^T Y with G symmetric in exact arithmetic: the Euclidean Gram
+// Z^T Z and the tridiagonal Z^T (T Z)), upper triangle only -- what K2 reads; the reduction then
+// mirrors it (launch_gram_reduce mode REDUCE_MIRROR).  The l-tile columns are cut into P parts
+// of nearly equal upper-triangle area; part p (columns [c_p, c_p+1)) needs only k-tiles
+// [0, c_p+1) of X, and of its 4 x 2 warp blocks those entirely below the diagonal are skipped.
+// Grid = K-slices x P.
+__host__ __device__ constexpr int upper_parts(int NT) { return NT >= 12 ? 4 : (NT >= 6 ? 2 : 1); }
+__host__ __device__ constexpr int upper_cut(int NT, int p) {
+  const int P = upper_parts(NT);
+  if (p <= 0) return 0;
+  if (p >= P) return NT;
+  const long long tot = (long long)NT * (NT + 1) / 2;
+  int best = 1;
+  long long bestd = -1;
+  for (int c = 1; c < NT; ++c) {
+    long long d = (long long)c * (c + 1) / 2 * P - (long long)p * tot;
+    if (d < 0) d = -d;
+    if (bestd < 0 || d < bestd) {
+      bestd = d;
+      best = c;
+    }
+  }
+  return best;
+}
+__host__ __device__ constexpr int upper_lmax(int NT) {
+  int w = 0;
+  for (int p = 0; p < upper_parts(NT); ++p)
+    if (upper_cut(NT, p + 1) - upper_cut(NT, p) > w) w = upper_cut(NT, p + 1) - upper_cut(NT, p);
+  return w;
+}
+
+template <int NT, int PART>
+__device__ __forceinline__ void packed_upper_part(double* ring, int STAGE, uint64_t* full, uint64_t* empty,
+                                                  unsigned* relcnt, int stages, int b0, int b1,
+                                                  const double* __restrict__ Xp, const double* __restrict__ Yp,
+                                                  double* slot, int warp, int lane, uint64_t pol) {
+  constexpr int c0 = upper_cut(NT, PART), c1 = upper_cut(NT, PART + 1);
+  constexpr int K = c1, L = c1 - c0;
+  constexpr int KH = (K + 3) / 4, KL = K / 4, LH = (L + 1) / 2, LL = L / 2;
+  const int wk = warp & 3, wl = warp >> 2;
+  const int kt0 = wk * K / 4, nkt = (wk + 1) * K / 4 - kt0;
+  const int lt0 = c0 + wl * L / 2, nlt = c0 + (wl + 1) * L / 2 - lt0;
+  const bool skip = kt0 >= lt0 + nlt;  // every k-tile of the block below every l-tile
+#define OQR_UPPER_BODY(KT_, LT_)                                                                               \
+  packed_gram_body<NT, KT_, LT_>(ring, STAGE, full, empty, relcnt, stages, b0, b1, kt0, lt0, c0, L, Xp, Yp, slot, \
+                                 lane, pol, c1)
+  if (skip) OQR_UPPER_BODY(0, 0);
+  else if (nkt == KH && nlt == LH) OQR_UPPER_BODY(KH, LH);
+  else if (nkt == KH) OQR_UPPER_BODY(KH, LL);
+  else if (nlt == LH) OQR_UPPER_BODY(KL, LH);
+  else OQR_UPPER_BODY(KL, LL);
+#undef OQR_UPPER_BODY
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256, 1)
+gram_packed_upper_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp, int nblk,
+                         double* __restrict__ P, int stages) {
+  constexpr int NP = NT * 8;
+  constexpr int STAGE = (NT + upper_lmax(NT)) * 4 * FRAG;  // X (first c_p+1 tiles used), Y part
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 8;
+  unsigned* relcnt = reinterpret_cast<unsigned*>(empty + 8);
+  double* ring = reinterpret_cast<double*>(smem + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slice = blockIdx.x, nslices = gridDim.x, part = blockIdx.y;
+  const int b0 = (int)((int64_t)nblk * slice / nslices), b1 = (int)((int64_t)nblk * (slice + 1) / nslices);
+  const int c0 = upper_cut(NT, part), c1 = upper_cut(NT, part + 1);
+  const uint64_t pol = policy_evict_last();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+      relcnt[s] = 0u;
+    }
+    mbar_fence_init();
+    for (int s = 0; s < stages && b0 + s < b1; ++s)
+      packed_issue<NT>(ring + s * STAGE, Xp, Yp, b0 + s, c0, c1 - c0, &full[s], pol, c1);
+  }
+  __syncthreads();
+  double* slot = P + (int64_t)slice * NP * NP;
+  switch (part) {
+    case 0: packed_upper_part<NT, 0>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
+    case 1: if (upper_parts(NT) > 1) packed_upper_part<NT, (upper_parts(NT) > 1 ? 1 : 0)>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
+    case 2: if (upper_parts(NT) > 2) packed_upper_part<NT, (upper_parts(NT) > 2 ? 2 : 0)>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
+    default: if (upper_parts(NT) > 3) packed_upper_part<NT, (upper_parts(NT) > 3 ? 3 : 0)>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
+  }
+}
+
 // ------------------------------------------------------------------ K1r -------------------
 // G[k, l] = sum_{c=0}^{g-1} P[c][l*NP + k], c ascending (fixed order => reproducible bits).
 // sym (NEXT-N4): G = T + T^T with T = sum_c P[c], i.e. G[k,l] = T[k,l] + T[l,k] (bitwise symmetric).
 __global__ void gram_reduce_kernel(int n, int NP, int g, const double* __restrict__ P,
-                                   double* __restrict__ G, int64_t ldg, bool sym) {
+                                   double* __restrict__ G, int64_t ldg, bool sym, bool mirror) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
   const int l = (int)(idx / n), k = (int)(idx - (int64_t)l * n);
   const int64_t stride = (int64_t)NP * NP;
-  const double* p = P + (int64_t)l * NP + k;
+  // mirror: the slots hold the upper triangle only (K4' upper): G[k,l] = G[l,k] = upper entry
+  const double* p = mirror ? P + (int64_t)max(k, l) * NP + min(k, l) : P + (int64_t)l * NP + k;
   double s = p[0];
   for (int c = 1; c < g; ++c) s += p[c * stride];
   if (sym) {
@@ -779,17 +871,18 @@ __global__ void gram_reduce_kernel(int n, int NP, int g, const double* __restric
   G[(int64_t)l * ldg + k] = s;
 }
 
-cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s, bool sym) {
+cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s, bool sym,
+                               bool mirror) {
   const int NP = 8 * (int)cdiv(n, 8);
   const int64_t total = (int64_t)n * n;
-  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, NP, g, P, G, ldg, sym);
+  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, NP, g, P, G, ldg, sym, mirror);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s) {
   const int64_t total = (int64_t)n * n;
-  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, n, count, P, G, ldg, false);
+  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, n, count, P, G, ldg, false, false);
   note_launch();
   return cudaGetLastError();
 }
@@ -934,6 +1027,30 @@ static cudaError_t gram_packed_nt(int64_t m, const double* Xp, const double* Yp,
   return e;
 }
 
+template <int NT>
+static cudaError_t gram_packed_upper_nt(int64_t m, const double* Xp, const double* Yp, double* P, int* g_out,
+                                        cudaStream_t s) {
+  constexpr int NCP = upper_parts(NT);
+  const size_t stage = (size_t)(NT + upper_lmax(NT)) * 4 * FRAG * 8;
+  int stages = (int)((SMEM_MAX - 256) / stage);
+  if (stages > 8) stages = 8;
+  const size_t bytes = 256 + stages * stage;
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_packed_upper_kernel<NT>), (int)bytes);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t nblk = zp_blocks(m);
+  int64_t nsl = num_sms() / NCP;
+  if (nsl > nblk) nsl = nblk;
+  *g_out = (int)nsl;
+  timing_begin(s, OQR_TIMING_K4);
+  gram_packed_upper_kernel<NT><<<dim3((unsigned)nsl, NCP), 256, bytes, s>>>(Xp, Yp, (int)nblk, P, stages);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  timing_end(s);
+  return e;
+}
+
 #define OQR_NT_CASES(X) \
   X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
@@ -954,10 +1071,10 @@ cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int
 }
 
 cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool upper) {
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT) \
-  case NT: return gram_packed_nt<NT>(m, Xp, Yp, P, g_out, s);
+  case NT: return upper ? gram_packed_upper_nt<NT>(m, Xp, Yp, P, g_out, s) : gram_packed_nt<NT>(m, Xp, Yp, P, g_out, s);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;
