@@ -2,7 +2,7 @@
 wrong index, transposed operand, wrong factor order) to oracle/oqr_oracle.c one at a time,
 rebuild, and confirm that tests/test_oracle_pins.py fails for each.  Restores the source.
 
-    python tools/oracle_mutation_check.py
+    python tests/oracle_mutation_check.py   (test infrastructure: not collected by pytest)
 """
 import os
 import shutil
