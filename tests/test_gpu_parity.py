@@ -499,3 +499,25 @@ def test_normal_host_argument_errors(oqr):
     assert L.oqr_normal_host(64, 8, P(A), 63, P(Z), 64, P(Q), P(R), 0, s) == -4
     assert L.oqr_normal_host(64, 8, P(A), 64, P(Z), 64, P(Q), P(R), -1, s) == -9
     assert L.oqr_normal_host(64, 65, P(A), 64, P(Z), 64, P(Q), P(R), 0, s) == -2
+
+
+# K4' upper-triangle variant: its column parts change at NT = 6 (2 parts) and NT = 12 (4 parts);
+# n on both sides of those boundaries and of the widest shapes, Euclidean and tridiagonal Grams
+# (T1; the mirrored lower triangle must equal the upper bitwise).
+@pytest.mark.parametrize("n", [40, 41, 48, 49, 88, 89, 96, 97, 232, 233])
+def test_t1_packed_upper_gram_part_boundaries(oqr, n):
+    m = 1000 + n
+    p = make(m, n, 1e2, 1e2, 70 + n)
+    Z = to_dev(p.Z)
+    G = host(oqr.gram_euclid(Z, m=m)).T
+    assert np.array_equal(G, G.T)
+    Go = oracle.from_cm(oracle.gram_euclid(p.Z, m), n)
+    Zd = oracle.from_cm(p.Z, m)
+    assert np.all(np.abs(G - Go) <= 2 * gamma(3 * m) * (np.abs(Zd).T @ np.abs(Zd)))
+    d, e = gen.tridiag(m, 1e3)
+    Gt = host(oqr.gram_tridiag(to_dev(d), to_dev(e), Z)).T
+    assert np.array_equal(Gt, Gt.T)
+    Got = oracle.from_cm(oracle.gram_tridiag(d, e, p.Z, m), n)
+    Td = np.abs(np.diag(d)) + np.abs(np.diag(e, 1)) + np.abs(np.diag(e, -1))
+    Mt = np.abs(Zd).T @ (Td @ np.abs(Zd))
+    assert np.all(np.abs(Gt - Got) <= 2 * gamma(m + 3) * Mt)
