@@ -759,93 +759,109 @@ gram_packed_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp,
                                            Xp, Yp, slot, lane, pol);
 }
 
-// K4' for a symmetric product (X^T Y with G symmetric in exact arithmetic: the Euclidean Gram
-// Z^T Z and the tridiagonal Z^T (T Z)), upper triangle only -- what K2 reads; the reduction then
-// mirrors it (launch_gram_reduce mode REDUCE_MIRROR).  The l-tile columns are cut into P parts
-// of nearly equal upper-triangle area; part p (columns [c_p, c_p+1)) needs only k-tiles
-// [0, c_p+1) of X, and of its 4 x 2 warp blocks those entirely below the diagonal are skipped.
-// Grid = K-slices x P.
-__host__ __device__ constexpr int upper_parts(int NT) { return NT >= 12 ? 4 : (NT >= 6 ? 2 : 1); }
-__host__ __device__ constexpr int upper_cut(int NT, int p) {
-  const int P = upper_parts(NT);
-  if (p <= 0) return 0;
-  if (p >= P) return NT;
-  const long long tot = (long long)NT * (NT + 1) / 2;
-  int best = 1;
-  long long bestd = -1;
-  for (int c = 1; c < NT; ++c) {
-    long long d = (long long)c * (c + 1) / 2 * P - (long long)p * tot;
-    if (d < 0) d = -d;
-    if (bestd < 0 || d < bestd) {
-      bestd = d;
-      best = c;
-    }
-  }
-  return best;
-}
-__host__ __device__ constexpr int upper_lmax(int NT) {
-  int w = 0;
-  for (int p = 0; p < upper_parts(NT); ++p)
-    if (upper_cut(NT, p + 1) - upper_cut(NT, p) > w) w = upper_cut(NT, p + 1) - upper_cut(NT, p);
-  return w;
-}
-
-template <int NT, int PART>
-__device__ __forceinline__ void packed_upper_part(double* ring, int STAGE, uint64_t* full, uint64_t* empty,
-                                                  unsigned* relcnt, int stages, int b0, int b1,
-                                                  const double* __restrict__ Xp, const double* __restrict__ Yp,
-                                                  double* slot, int warp, int lane, uint64_t pol) {
-  constexpr int c0 = upper_cut(NT, PART), c1 = upper_cut(NT, PART + 1);
-  constexpr int K = c1, L = c1 - c0;
-  constexpr int KH = (K + 3) / 4, KL = K / 4, LH = (L + 1) / 2, LL = L / 2;
-  const int wk = warp & 3, wl = warp >> 2;
-  const int kt0 = wk * K / 4, nkt = (wk + 1) * K / 4 - kt0;
-  const int lt0 = c0 + wl * L / 2, nlt = c0 + (wl + 1) * L / 2 - lt0;
-  const bool skip = kt0 >= lt0 + nlt;  // every k-tile of the block below every l-tile
-#define OQR_UPPER_BODY(KT_, LT_)                                                                               \
-  packed_gram_body<NT, KT_, LT_>(ring, STAGE, full, empty, relcnt, stages, b0, b1, kt0, lt0, c0, L, Xp, Yp, slot, \
-                                 lane, pol, c1)
-  if (skip) OQR_UPPER_BODY(0, 0);
-  else if (nkt == KH && nlt == LH) OQR_UPPER_BODY(KH, LH);
-  else if (nkt == KH) OQR_UPPER_BODY(KH, LL);
-  else if (nlt == LH) OQR_UPPER_BODY(KL, LH);
-  else OQR_UPPER_BODY(KL, LL);
-#undef OQR_UPPER_BODY
-}
+// K4' for a symmetric product (X^T Y, G symmetric in exact arithmetic: the Euclidean Gram Z^T Z
+// and the tridiagonal Z^T (T Z)), upper triangle only -- what K2 reads; the reduction then
+// mirrors it (launch_gram_reduce(..., mirror = true)).  Tile row i of the upper triangle holds
+// NT - i tiles, so rows i and NT-1-i together hold NT + 1: each such pair is split into two
+// warps of ceil((NT+1)/2) tiles (the first: a prefix of row i; the second: the rest of row i and
+// all of row NT-1-i), plus the middle row when NT is odd -- NT warps with equal work and no tile
+// outside the triangle.  One or two CTA parts of those warps (registers: NT <= 25 fit in one
+// CTA of 32 NT threads) x K-slices; every CTA streams its block range of Xp and Yp once.
+__host__ __device__ constexpr int pairs_parts(int NT) { return NT <= 25 ? 1 : 2; }
+__host__ __device__ constexpr int pairs_tiles(int NT) { return (NT + 2) / 2; }  // ceil((NT + 1) / 2)
+__host__ __device__ constexpr int pairs_warps(int NT) { return (NT + pairs_parts(NT) - 1) / pairs_parts(NT); }
 
 template <int NT>
-__global__ void __launch_bounds__(256, 1)
-gram_packed_upper_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp, int nblk,
+__global__ void __launch_bounds__(32 * pairs_warps(NT), 1)
+gram_packed_pairs_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp, int nblk,
                          double* __restrict__ P, int stages) {
   constexpr int NP = NT * 8;
-  constexpr int STAGE = (NT + upper_lmax(NT)) * 4 * FRAG;  // X (first c_p+1 tiles used), Y part
+  constexpr int T = pairs_tiles(NT);
+  constexpr int NW = pairs_warps(NT);
+  constexpr int STAGE = 2 * NT * 4 * FRAG;  // the block's X and Y tiles
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
   unsigned* relcnt = reinterpret_cast<unsigned*>(empty + 8);
   double* ring = reinterpret_cast<double*>(smem + 256);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slice = blockIdx.x, nslices = gridDim.x, part = blockIdx.y;
+  const int slice = blockIdx.x, nslices = gridDim.x;
   const int b0 = (int)((int64_t)nblk * slice / nslices), b1 = (int)((int64_t)nblk * (slice + 1) / nslices);
-  const int c0 = upper_cut(NT, part), c1 = upper_cut(NT, part + 1);
   const uint64_t pol = policy_evict_last();
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
+      mbar_init(&empty[s], NW);
       relcnt[s] = 0u;
     }
     mbar_fence_init();
     for (int s = 0; s < stages && b0 + s < b1; ++s)
-      packed_issue<NT>(ring + s * STAGE, Xp, Yp, b0 + s, c0, c1 - c0, &full[s], pol, c1);
+      packed_issue<NT>(ring + s * STAGE, Xp, Yp, b0 + s, 0, NT, &full[s], pol);
   }
   __syncthreads();
+  // this warp's tiles: t < len1 -> (ka, la0 + t); len1 <= t < len -> (kb, lb0 + t - len1)
+  const int g = blockIdx.y * NW + warp;  // global warp index, 0 .. NT - 1 (>= NT: ring hand-off only)
+  int ka = 0, la0 = 0, len1 = 0, kb = 0, lb0 = 0, len = 0;
+  if (g < NT) {
+    const int i = g >> 1;
+    if ((NT & 1) && g == NT - 1) {  // middle row
+      ka = i; la0 = i; len1 = len = NT - i;
+    } else if ((g & 1) == 0) {      // prefix of row i
+      ka = i; la0 = i; len1 = len = T;
+    } else {                        // rest of row i, then row NT-1-i
+      ka = i; la0 = i + T; len1 = NT - i - T;
+      kb = NT - 1 - i; lb0 = NT - 1 - i; len = len1 + i + 1;
+    }
+  }
+  double acc[T][2];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int b = b0; b < b1; ++b) {
+    mbar_wait(&full[s], ph);
+    const double* Xs = ring + s * STAGE + lane;
+    const double* Ys = Xs + NT * 4 * FRAG;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const double xa = Xs[(ka * 4 + kk) * FRAG];
+      const double xb = Xs[(kb * 4 + kk) * FRAG];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        if (t < len) {
+          const int l = t < len1 ? la0 + t : lb0 + (t - len1);
+          dmma(acc[t], t < len1 ? xa : xb, Ys[(l * 4 + kk) * FRAG]);
+        }
+      }
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      mbar_arrive(&empty[s]);
+      last = (atomicAdd(&relcnt[s], 1u) % NW) == NW - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && b + stages < b1) {
+      mbar_wait(&empty[s], ph);
+      if (lane == 0) packed_issue<NT>(ring + s * STAGE, Xp, Yp, b + stages, 0, NT, &full[s], pol);
+      __syncwarp();
+    }
+    if (++s == stages) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+  // C tile t: rows k*8 + lane/4, cols l*8 + 2*(lane%4) + e
   double* slot = P + (int64_t)slice * NP * NP;
-  switch (part) {
-    case 0: packed_upper_part<NT, 0>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
-    case 1: if (upper_parts(NT) > 1) packed_upper_part<NT, (upper_parts(NT) > 1 ? 1 : 0)>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
-    case 2: if (upper_parts(NT) > 2) packed_upper_part<NT, (upper_parts(NT) > 2 ? 2 : 0)>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
-    default: if (upper_parts(NT) > 3) packed_upper_part<NT, (upper_parts(NT) > 3 ? 3 : 0)>(ring, STAGE, full, empty, relcnt, stages, b0, b1, Xp, Yp, slot, warp, lane, pol); break;
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    if (t < len) {
+      const int k = t < len1 ? ka : kb;
+      const int l = t < len1 ? la0 + t : lb0 + (t - len1);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        slot[(int64_t)(l * 8 + 2 * (lane & 3) + e) * NP + k * 8 + (lane >> 2)] = acc[t][e];
+    }
   }
 }
 
@@ -1030,13 +1046,13 @@ static cudaError_t gram_packed_nt(int64_t m, const double* Xp, const double* Yp,
 template <int NT>
 static cudaError_t gram_packed_upper_nt(int64_t m, const double* Xp, const double* Yp, double* P, int* g_out,
                                         cudaStream_t s) {
-  constexpr int NCP = upper_parts(NT);
-  const size_t stage = (size_t)(NT + upper_lmax(NT)) * 4 * FRAG * 8;
+  constexpr int NCP = pairs_parts(NT);
+  const size_t stage = (size_t)2 * NT * 4 * FRAG * 8;
   int stages = (int)((SMEM_MAX - 256) / stage);
   if (stages > 8) stages = 8;
   const size_t bytes = 256 + stages * stage;
   {
-    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_packed_upper_kernel<NT>), (int)bytes);
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_packed_pairs_kernel<NT>), (int)bytes);
     if (e != cudaSuccess) return e;
   }
   const int64_t nblk = zp_blocks(m);
@@ -1044,7 +1060,8 @@ static cudaError_t gram_packed_upper_nt(int64_t m, const double* Xp, const doubl
   if (nsl > nblk) nsl = nblk;
   *g_out = (int)nsl;
   timing_begin(s, OQR_TIMING_K4);
-  gram_packed_upper_kernel<NT><<<dim3((unsigned)nsl, NCP), 256, bytes, s>>>(Xp, Yp, (int)nblk, P, stages);
+  gram_packed_pairs_kernel<NT><<<dim3((unsigned)nsl, NCP), 32 * pairs_warps(NT), bytes, s>>>(Xp, Yp, (int)nblk, P,
+                                                                                           stages);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);
