@@ -256,7 +256,7 @@ def bench_tridiag(args):
                    "m": m, "n": n, "variant": args.variant, "flops_per_step": fl,
                    "flop_normalisation": "2mn^2 (PAPER.md:960-961)",
                    "l2": "Z = %.0f MB, packed Z and T Z = %.0f MB > L2; no flush" % (8e-6 * m * n, 128e-6 * m * NT)},
-        "roofline": {"bound": "tensor", "kernel": "gram_packed_upper (K4'): upper triangle of G = Z^T (T Z)",
+        "roofline": {"bound": "tensor", "kernel": "gram_packed_pairs (K4'): upper triangle of G = Z^T (T Z)",
                      "achieved": achieved,
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
                      "traffic": traffic, "algorithmic_flops_per_launch": fl_k4, "mean_launch_ms": k4_ms,
