@@ -119,6 +119,75 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 // ------------------------------------------------------------------ Z packing -------------
 // Zp[((b*NT + lt)*4 + kk)*32 + ln] = Z[b*BK + kk*4 + ln%4, lt*8 + ln/4] (zero outside Z).
+// Packing through shared memory: a CTA stages a 64-row x 32-column tile of Z (plus one halo row
+// above and below for the stencil) with coalesced column reads, then writes the tile's 4 x 4
+// fragment groups of Zp (and W = T Z) as contiguous 1 KiB runs.  TRI: also W, w_il =
+// e_{i-1} z_{i-1,l} + d_i z_il + e_i z_{i+1,l} (fma order as the per-element kernel).
+constexpr int PT_R = 64, PT_C = 32;
+template <bool TRI>
+__global__ void __launch_bounds__(256)
+pack_tile_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t ldz, double* __restrict__ Zp,
+                 double* __restrict__ Wp, const double* __restrict__ d, const double* __restrict__ e, double scale,
+                 int64_t nrt) {
+  __shared__ double zs[PT_C][PT_R + 3];
+  __shared__ double ds[PT_R], es[PT_R + 1];
+  const int nct = (NT * 8 + PT_C - 1) / PT_C;
+  for (int64_t tile = blockIdx.x; tile < nrt * nct; tile += gridDim.x) {
+    const int64_t rt = tile / nct;
+    const int ct = (int)(tile - rt * nct);
+    const int64_t r0 = rt * PT_R;
+    const int c0 = ct * PT_C;
+    __syncthreads();  // previous tile's readers are done
+    {  // all of this thread's loads in flight before the first shared-memory store
+      constexpr int NQ = (PT_C * (PT_R + 2) + 255) / 256;
+      double v[NQ];
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        const int q = threadIdx.x + u * 256;
+        const int c = q / (PT_R + 2), rr = q - c * (PT_R + 2);
+        const int64_t row = r0 + rr - 1;
+        const int col = c0 + c;
+        v[u] = (q < PT_C * (PT_R + 2) && row >= 0 && row < m && col < n) ? Z[(int64_t)col * ldz + row] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        const int q = threadIdx.x + u * 256;
+        if (q < PT_C * (PT_R + 2)) zs[q / (PT_R + 2)][q % (PT_R + 2)] = v[u];
+      }
+    }
+    if (TRI) {
+      for (int q = threadIdx.x; q < PT_R + 1; q += blockDim.x) {
+        const int64_t row = r0 + q - 1;  // es[q] = e_{r0+q-1} (the coupling of rows r0+q-1, r0+q)
+        es[q] = (row >= 0 && row < m - 1) ? e[row] : 0.0;
+        if (q < PT_R) ds[q] = (r0 + q < m) ? d[r0 + q] : 0.0;
+      }
+    }
+    __syncthreads();
+    // 4 row blocks x 4 column tiles, 128 doubles each: o -> (block, tile, kk, lane)
+    for (int o = threadIdx.x; o < (PT_R / BK) * (PT_C / 8) * 4 * FRAG; o += blockDim.x) {
+      const int grp = o >> 7, w = o & 127;
+      const int bl = grp >> 2, tl = grp & 3;
+      const int kk = w >> 5, ln = w & 31;
+      const int r = bl * BK + kk * 4 + (ln & 3);  // tile-local row
+      const int c = tl * 8 + (ln >> 2);           // tile-local column
+      const int64_t b = r0 / BK + bl;
+      const int lt = c0 / 8 + tl;
+      if (lt >= NT) continue;
+      const int64_t dst = ((b * NT + lt) * 4 + kk) * FRAG + ln;
+      const double zv = zs[c][r + 1];
+      if (TRI) {
+        double wv = es[r] * zs[c][r];
+        wv = fma(ds[r], zv, wv);
+        wv = fma(es[r + 1], zs[c][r + 2], wv);
+        Zp[dst] = zv;
+        Wp[dst] = (r0 + r < m) ? wv : 0.0;
+      } else {
+        Zp[dst] = scale * zv;
+      }
+    }
+  }
+}
+
 __global__ void pack_z_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t ldz,
                               double* __restrict__ Zp, int64_t total, double scale) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -142,7 +211,11 @@ cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double
   const int64_t total = zp_doubles(m, 8 * NT);
   int64_t blocks = cdiv(total, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  pack_z_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, n, NT, Z, ldz, Zp, total, scale);
+  (void)blocks;
+  const int64_t nrt = cdiv(zp_blocks(m) * BK, PT_R);  // Zp is padded to whole 64-row panels
+  int64_t grid = nrt * cdiv(NT * 8, PT_C);
+  if (grid > 148 * 8) grid = 148 * 8;
+  pack_tile_kernel<false><<<(unsigned)grid, 256, 0, s>>>(m, n, NT, Z, ldz, Zp, nullptr, nullptr, nullptr, scale, nrt);
   note_launch();
   return cudaGetLastError();
 }
@@ -182,7 +255,12 @@ cudaError_t launch_pack_zw_tridiag(int64_t m, int n, const double* d, const doub
   const int64_t total = zp_doubles(m, 8 * NT);
   int64_t blocks = cdiv(total, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  pack_zw_tridiag_kernel<<<(unsigned)blocks, 256, 0, s>>>(m, n, NT, d, e, Z, ldz, Zp, Wp, total);
+  (void)blocks;
+  (void)total;
+  const int64_t nrt = cdiv(zp_blocks(m) * BK, PT_R);
+  int64_t grid = nrt * cdiv(NT * 8, PT_C);
+  if (grid > 148 * 8) grid = 148 * 8;
+  pack_tile_kernel<true><<<(unsigned)grid, 256, 0, s>>>(m, n, NT, Z, ldz, Zp, Wp, d, e, 1.0, nrt);
   note_launch();
   return cudaGetLastError();
 }
@@ -869,36 +947,68 @@ gram_packed_pairs_kernel(const double* __restrict__ Xp, const double* __restrict
 // G[k, l] = sum_{c=0}^{g-1} P[c][l*NP + k], c ascending (fixed order => reproducible bits).
 // sym (NEXT-N4): G = T + T^T with T = sum_c P[c], i.e. G[k,l] = T[k,l] + T[l,k] (bitwise symmetric).
 __global__ void gram_reduce_kernel(int n, int NP, int g, const double* __restrict__ P,
-                                   double* __restrict__ G, int64_t ldg, bool sym, bool mirror) {
+                                   double* __restrict__ G, int64_t ldg, bool mirror) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)n * n) return;
-  const int l = (int)(idx / n), k = (int)(idx - (int64_t)l * n);
-  const int64_t stride = (int64_t)NP * NP;
-  // mirror: the slots hold the upper triangle only (K4' upper): G[k,l] = G[l,k] = upper entry
-  const double* p = mirror ? P + (int64_t)max(k, l) * NP + min(k, l) : P + (int64_t)l * NP + k;
-  double s = p[0];
-  for (int c = 1; c < g; ++c) s += p[c * stride];
-  if (sym) {
-    const double* q = P + (int64_t)k * NP + l;
-    double t = q[0];
-    for (int c = 1; c < g; ++c) t += q[c * stride];
-    s = (k <= l) ? s + t : t + s;  // same operand order for (k,l) and (l,k)
+  int k, l;
+  if (mirror) {  // one thread per upper entry k <= l (packed column order: coalesced slot reads)
+    if (idx >= (int64_t)n * (n + 1) / 2) return;
+    l = (int)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
+    while ((int64_t)l * (l + 1) / 2 > idx) --l;
+    while ((int64_t)(l + 1) * (l + 2) / 2 <= idx) ++l;
+    k = (int)(idx - (int64_t)l * (l + 1) / 2);
+  } else {
+    if (idx >= (int64_t)n * n) return;
+    l = (int)(idx / n);
+    k = (int)(idx - (int64_t)l * n);
   }
+  const int64_t stride = (int64_t)NP * NP;
+  const double* p = P + (int64_t)l * NP + k;
+  // c ascending; loads issued eight at a time, added in order (the same bits as a plain loop)
+  double s = p[0];
+  int c = 1;
+  for (; c + 8 <= g; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = p[(int64_t)(c + u) * stride];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; c < g; ++c) s += p[(int64_t)c * stride];
   G[(int64_t)l * ldg + k] = s;
+  if (mirror && k != l) G[(int64_t)k * ldg + l] = s;
+}
+
+// sym (NEXT-N4): G holds T = sum_c P[c]; G[k,l] = G[l,k] = T[k,l] + T[l,k] for k <= l (the
+// operand order of both entries is the upper one: bitwise symmetric).  One thread per pair.
+__global__ void gram_symmetrize_kernel(int n, double* __restrict__ G, int64_t ldg) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * (n + 1) / 2) return;
+  int l = (int)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
+  while ((int64_t)l * (l + 1) / 2 > idx) --l;
+  while ((int64_t)(l + 1) * (l + 2) / 2 <= idx) ++l;
+  const int k = (int)(idx - (int64_t)l * (l + 1) / 2);
+  const double v = G[(int64_t)l * ldg + k] + G[(int64_t)k * ldg + l];
+  G[(int64_t)l * ldg + k] = v;
+  G[(int64_t)k * ldg + l] = v;
 }
 
 cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s, bool sym,
                                bool mirror) {
   const int NP = 8 * (int)cdiv(n, 8);
-  const int64_t total = (int64_t)n * n;
-  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, NP, g, P, G, ldg, sym, mirror);
+  const int64_t total = mirror ? (int64_t)n * (n + 1) / 2 : (int64_t)n * n;
+  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, NP, g, P, G, ldg, mirror);
   note_launch();
+  if (sym) {
+    const int64_t pairs = (int64_t)n * (n + 1) / 2;
+    gram_symmetrize_kernel<<<(unsigned)cdiv(pairs, 128), 128, 0, s>>>(n, G, ldg);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, int64_t ldg, cudaStream_t s) {
   const int64_t total = (int64_t)n * n;
-  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, n, count, P, G, ldg, false, false);
+  gram_reduce_kernel<<<(unsigned)cdiv(total, 128), 128, 0, s>>>(n, n, count, P, G, ldg, false);
   note_launch();
   return cudaGetLastError();
 }
