@@ -188,30 +188,8 @@ pack_tile_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t
   }
 }
 
-__global__ void pack_z_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t ldz,
-                              double* __restrict__ Zp, int64_t total, double scale) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int ln = (int)(e & 31);
-    const int64_t f = e >> 5;
-    const int kk = (int)(f & 3);
-    const int64_t bl = f >> 2;
-    const int lt = (int)(bl % NT);
-    const int64_t b = bl / NT;
-    const int64_t row = b * BK + kk * 4 + (ln & 3);
-    const int col = lt * 8 + (ln >> 2);
-    double v = 0.0;
-    if (row < m && col < n) v = scale * Z[(int64_t)col * ldz + row];  // scale: 1 or 1/2 (exact)
-    Zp[e] = v;
-  }
-}
-
 cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double* Zp, cudaStream_t s, double scale) {
   const int NT = (int)cdiv(n, 8);
-  const int64_t total = zp_doubles(m, 8 * NT);
-  int64_t blocks = cdiv(total, 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  (void)blocks;
   const int64_t nrt = cdiv(zp_blocks(m) * BK, PT_R);  // Zp is padded to whole 64-row panels
   int64_t grid = nrt * cdiv(NT * 8, PT_C);
   if (grid > 148 * 8) grid = 148 * 8;
@@ -221,42 +199,10 @@ cudaError_t launch_pack_z(int64_t m, int n, const double* Z, int64_t ldz, double
 }
 
 // Zp and W = T Z for T = tridiag(e, d, e) (NEXT-N3) in one pass over Z, both written straight into
-// the packed fragment order (the A and B operands of the packed Gram kernel):
-//   w_il = e_{i-1} z_{i-1,l} + d_i z_il + e_i z_{i+1,l}.
-__global__ void pack_zw_tridiag_kernel(int64_t m, int n, int NT, const double* __restrict__ d,
-                                       const double* __restrict__ e, const double* __restrict__ Z, int64_t ldz,
-                                       double* __restrict__ Zp, double* __restrict__ Wp, int64_t total) {
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int ln = (int)(idx & 31);
-    const int64_t f = idx >> 5;
-    const int kk = (int)(f & 3);
-    const int64_t bl = f >> 2;
-    const int lt = (int)(bl % NT);
-    const int64_t b = bl / NT;
-    const int64_t row = b * BK + kk * 4 + (ln & 3);
-    const int col = lt * 8 + (ln >> 2);
-    double zv = 0.0, w = 0.0;
-    if (row < m && col < n) {
-      const double* z = Z + (int64_t)col * ldz;
-      zv = z[row];
-      if (row > 0) w = e[row - 1] * z[row - 1];
-      w = fma(d[row], zv, w);
-      if (row < m - 1) w = fma(e[row], z[row + 1], w);
-    }
-    Zp[idx] = zv;
-    Wp[idx] = w;
-  }
-}
-
+// the packed fragment order (the A and B operands of the packed Gram kernel): pack_tile_kernel<true>.
 cudaError_t launch_pack_zw_tridiag(int64_t m, int n, const double* d, const double* e, const double* Z, int64_t ldz,
                                    double* Zp, double* Wp, cudaStream_t s) {
   const int NT = (int)cdiv(n, 8);
-  const int64_t total = zp_doubles(m, 8 * NT);
-  int64_t blocks = cdiv(total, 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  (void)blocks;
-  (void)total;
   const int64_t nrt = cdiv(zp_blocks(m) * BK, PT_R);
   int64_t grid = nrt * cdiv(NT * 8, PT_C);
   if (grid > 148 * 8) grid = 148 * 8;
