@@ -250,7 +250,10 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 
 // Warps per CTA: as many as the per-tile register accumulators allow without spills (ptxas:
 // 16 warps <= 128 registers up to NT = 16, 12 warps <= 168 up to NT = 29, else 8).
-__host__ __device__ constexpr int trsm_threads(int NT) { return NT <= 16 ? 512 : (NT <= 29 ? 384 : 256); }
+#ifndef OQR_EXP_TRSM_T16
+#define OQR_EXP_TRSM_T16 16
+#endif
+__host__ __device__ constexpr int trsm_threads(int NT) { return NT <= OQR_EXP_TRSM_T16 ? 512 : (NT <= 29 ? 384 : 256); }
 
 template <int NT>
 constexpr size_t trsm_smem_doubles(bool with_rd) {
