@@ -11,10 +11,12 @@
 //
 // FP64 has no tcgen05 kind on sm_100a (ptxas rejects .kind::f64); the FP64 tensor pipe is
 // reached through warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Operands are staged in
-// shared memory through an mbarrier ring: the A tile (64 rows x 16 columns) by ONE 2-D tensor
-// TMA request (SASS UTMALDG; out-of-bounds rows/columns are zero-filled by the hardware), the
-// packed Z block by one 1-D bulk copy (SASS UBLKCP).  16 warps per CTA (8 row groups x 2
-// column halves) keep W_I in DMMA accumulators.
+// shared memory through an mbarrier ring: the A tile (64 rows x KS = 32 or 64 columns) by ONE
+// tensor TMA request over a 4-D view of A that lands it bank-conflict-free (SASS UTMALDG;
+// out-of-bounds rows/columns are zero-filled by the hardware; see ALAY_*), the packed Z block by
+// one 1-D bulk copy (SASS UBLKCP).  16 warps per CTA (8 row groups x 2 column halves) keep W_I
+// in DMMA accumulators.  Also here: K4' (packed tall-skinny Grams, full and upper-triangle),
+// the tiled packing kernel and K1r.
 #include <cuda.h>  // CUtensorMap and its enums (the encode entry point is fetched at run time)
 
 #include <cstdlib>

@@ -15,7 +15,7 @@ namespace oqr {
 
 // ---- Tiling of the fused Gram kernel (K1) and its packed Z layout ----------
 constexpr int BM = 64;        // rows of A (and of W = AZ) per panel: NRG row groups x 8 rows
-constexpr int BK = 16;        // columns of A (k of AZ) per pipeline stage
+constexpr int BK = 16;        // rows of Z per packed block (a K1 stage moves KS/BK of them)
 constexpr int NRG = 8;        // row groups per panel: 8 rows each (BM = 8 * NRG)
 constexpr int NCH = 2;        // column halves: warp (rg, ch) owns rows rg*8.. and half the n-tiles
 constexpr int NCW = NRG * NCH;  // 16 DMMA warps per CTA (4 per SM sub-partition)
