@@ -136,6 +136,37 @@ def cpu_oracle_sample(p, target_s: float = 12.0, lead=None):
                       f"first {r} rows of Z (n={n}); {dt:.1f} s; OMP threads={threads}"}, r, dt
 
 
+def oracle_protocol(configs):
+    """SURVEY s8(d) CPU-oracle timing protocol (informational, not the driver's JSON line): each
+    config's oracle oqr_normal, best of 3 (1 when a run exceeds 30 s), all host threads; c0 and c1
+    also single-threaded; inputs generated outside the timed region.  Prints one JSON line per
+    (config, threads)."""
+    import oracle
+    import ctypes
+    oracle.build()
+    model = next((l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")), "?")
+    allt = len(os.sched_getaffinity(0))
+    for k in configs:
+        p = gen.config(k)
+        for threads in ([allt, 1] if k in (0, 1) else [allt]):
+            os.environ["OMP_NUM_THREADS"] = str(threads)
+            try:  # the oracle's OpenMP runtime is already loaded: set its thread count directly
+                ctypes.CDLL("libgomp.so.1").omp_set_num_threads(threads)
+            except OSError:
+                pass
+            best = float("inf")
+            for _ in range(3):
+                t = time.perf_counter()
+                _, _, st = oracle.normal(p.A, p.Z, p.m)
+                dt = time.perf_counter() - t
+                best = min(best, dt)
+                if dt > 30.0:
+                    break
+            print(json.dumps({"oracle": "normal", "config": k, "m": p.m, "n": p.n, "threads": threads,
+                              "cpu": model, "best_s": best, "status": st,
+                              "gflops": flops_paper(p.m, p.n) / best / 1e9}), flush=True)
+
+
 def reference_arm(args, cfg, rank):
     if rank != 0:
         return
@@ -297,6 +328,8 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--variant", default="normal", choices=["normal", "normal2", "prequr"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--oracle-protocol", default=None, metavar="CONFIGS",
+                    help="SURVEY s8(d) CPU-oracle timing for the given configs (e.g. 0,1,4,2,3) and exit")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sym", action="store_true",
@@ -313,6 +346,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.oracle_protocol is not None:
+        if rank == 0:
+            oracle_protocol([int(c) for c in args.oracle_protocol.split(",")])
+        return
     if args.impl == "reference":
         reference_arm(args, args.config, rank)
         return
