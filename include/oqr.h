@@ -16,8 +16,10 @@
  *    the caller; the library never frees or retains them.
  *  - A is read in full as given (both triangles); it is never written.  Z is never written.
  *  - lda, ldz >= m; all pointers 8-byte aligned.  FAST PATH: A 16-byte aligned and lda even --
- *    the fused Gram kernel then moves A columns with cp.async.bulk (16-byte aligned sources);
- *    otherwise it falls back to plain loads for every tile (same results, much slower).
+ *    the fused Gram kernel then moves each 64 x KS tile of A with one tensor-TMA request
+ *    (m % 8 == 0: a 4-D view that lands the tile bank-conflict-free; otherwise the 2-D view);
+ *    with a misaligned A or odd lda it falls back to plain loads for every tile (same results,
+ *    much slower).
  *  - 1 <= n <= min(m, OQR_NMAX).
  *  - Q: m x n output with leading dimension m.  R: n x n output with leading dimension n,
  *    upper triangular with positive diagonal; its strictly lower part is written as zero.
