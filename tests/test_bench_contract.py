@@ -1,0 +1,45 @@
+"""The bench.py JSON-line contract, checked on the recorded round-1 lines in profiles/ (CPU: no
+GPU needed): every key the driver and the judge read is present and consistent."""
+import json
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LINES = ["r01_bench_c3_normal.json", "r01_bench_c3_normal_sym.json", "r01_bench_tridiag_normal.json"]
+
+
+@pytest.mark.parametrize("name", LINES)
+def test_bench_line_has_the_contract_keys(name):
+    d = json.loads(open(os.path.join(ROOT, "profiles", name)).read().strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["dtype"] == "f64" and d["data"] == "synthetic" and d["higher_is_better"] is True
+    assert d["warmup"] >= 3 and d["n_gpus"] >= 1 and d["gpu_launches"] > 0
+    assert "workload" in d["config"]
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and 0 < r["frac"] <= 1
+    c = d["cpu_baseline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in c, k
+    assert c["kind"] == "oracle"
+    e = d["e2e"]
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in e, k
+    assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] < d["value"]
+    clk = d["clocks"]
+    assert clk["sm_mhz"] and clk["sm_max_mhz"] and not {"hw_slowdown", "hw_thermal_slowdown",
+                                                         "sw_thermal_slowdown"} & set(clk["reasons"])
+    # value is the whole-step rate: flops per step / ms per step
+    fl = d["config"]["flops_per_step"]
+    assert abs(d["value"] - fl / (d["ms_per_step"] * 1e-3) / 1e9) / d["value"] < 1e-6
+
+
+def test_reference_line():
+    d = json.loads(open(os.path.join(ROOT, "profiles", "r01_bench_reference.json")).read().strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
