@@ -43,3 +43,11 @@ def test_reference_line():
     d = json.loads(open(os.path.join(ROOT, "profiles", "r01_bench_reference.json")).read().strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_bench_metric_is_baselines():
+    import ast
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    metric = next(ast.literal_eval(n.value) for n in ast.parse(src).body
+                  if isinstance(n, ast.Assign) and getattr(n.targets[0], "id", "") == "METRIC")
+    assert metric == json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
