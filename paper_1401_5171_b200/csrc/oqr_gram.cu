@@ -534,7 +534,10 @@ __device__ __forceinline__ void consume_units(const CUtensorMap* tmap, int64_t m
     // trip is off the per-unit critical path; the refill lands stages - 2 units ahead.  Only for
     // NT <= 16 (short stages, where that round trip matters): the five extra live registers
     // would make the NT > 22 instantiations spill.
-    constexpr bool DEFER = NT <= 16;
+#ifndef OQR_EXP_DEFER_NT
+#define OQR_EXP_DEFER_NT 16
+#endif
+    constexpr bool DEFER = NT <= OQR_EXP_DEFER_NT;
     if (!DEFER) {
       __syncwarp();
       unsigned cnt = 0u;
