@@ -197,7 +197,7 @@ static int gram_into(const AOp& op, int64_t m, int n, const double* Z, int64_t l
   if (op.tridiag) {
     OQR_TRY(launch_pack_zw_tridiag(m, n, op.d, op.e, Z, ldz, ws.Zp, ws.Zc, s));
     // G = Z^T (T Z) is symmetric: upper tiles only, mirrored by the reduction
-    OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zc, ws.P, &g, s, true));
+    OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zc, ws.P, &g, s));
     OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s, false, true));
     return 0;
   }
@@ -216,7 +216,7 @@ static int gram_euclid_into(int64_t m, int n, const double* Z, int64_t ldz, doub
                             cudaStream_t s) {
   int g = 0;
   OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
-  OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zp, ws.P, &g, s, true));  // Z^T Z: upper tiles, mirrored
+  OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zp, ws.P, &g, s));  // Z^T Z: upper tiles, mirrored
   OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s, false, true));
   return 0;
 }

@@ -663,11 +663,10 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
 // Tall-skinny Gram of two packed operands: G = sum_b Xp_b^T Yp_b over 16-row blocks b, with Xp,
 // Yp in the DMMA fragment order of Zp (which is simultaneously the A-operand layout of X^T and
 // the B-operand layout of Y).  Used for the Euclidean Gram Z^T Z of the PRE-CHOLQR pre-step
-// (X = Y = Z, reading R2) and for the tridiagonal Gram Z^T (T Z) (Y = T Z, NEXT-N3).
-// Grid = K-slices x 2 (3 for n > 224) output column parts; CTA (slice, part) streams its block
-// range once (X: all NT tiles, Y: its half's tiles, one bulk copy each per block, mbarrier
-// ring) and 8 warps (4 along k-tiles x 2 along l-tiles) own disjoint output tiles in DMMA
-// accumulators, so no cross-warp reduction is needed; the slot of the slice is written once.
+// (X = Y = Z, reading R2) and for the tridiagonal Gram Z^T (T Z) (Y = T Z, NEXT-N3); both are
+// symmetric, so only the upper triangle is formed (gram_packed_pairs_kernel below).  A CTA
+// streams its block range once (X and Y, one bulk copy each per block, mbarrier ring); warps own
+// disjoint output tiles in DMMA accumulators, so the slot of the K-slice is written once.
 template <int NT>
 __device__ __forceinline__ void packed_issue(double* dst, const double* __restrict__ Xp, const double* __restrict__ Yp,
                                             int bn, int hl0, int NTH, uint64_t* bar, uint64_t pol, int NX = NT) {
@@ -675,117 +674,6 @@ __device__ __forceinline__ void packed_issue(double* dst, const double* __restri
   mbar_arrive_expect_tx(bar, xb + yb);
   bulk_g2s(dst, Xp + (int64_t)bn * NT * 4 * FRAG, xb, bar, pol);
   if (yb) bulk_g2s(dst + NT * 4 * FRAG, Yp + ((int64_t)bn * NT + hl0) * 4 * FRAG, yb, bar, pol);
-}
-
-// KT x LT output tiles per warp (compile time, either may be 0: the warp then only takes part in
-// the ring hand-off).
-template <int NT, int KT, int LT>
-__device__ __forceinline__ void packed_gram_body(double* ring, int STAGE, uint64_t* full, uint64_t* empty,
-                                                 unsigned* relcnt, int stages, int b0, int b1, int kt0, int lt0,
-                                                 int hl0, int NTH, const double* __restrict__ Xp,
-                                                 const double* __restrict__ Yp, double* slot, int lane, uint64_t pol,
-                                                 int NX = NT) {
-  constexpr int NP = NT * 8;
-  double acc[KT > 0 ? KT : 1][LT > 0 ? LT : 1][2];
-#pragma unroll
-  for (int i = 0; i < KT; ++i)
-#pragma unroll
-    for (int j = 0; j < LT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  int s = 0;
-  uint32_t ph = 0;
-  for (int b = b0; b < b1; ++b) {
-    mbar_wait(&full[s], ph);
-    const double* Xs = ring + s * STAGE + kt0 * 4 * FRAG + lane;
-    const double* Ys = ring + s * STAGE + NT * 4 * FRAG + (lt0 - hl0) * 4 * FRAG + lane;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[KT > 0 ? KT : 1], bb[LT > 0 ? LT : 1];
-#pragma unroll
-      for (int i = 0; i < KT; ++i) a[i] = Xs[(i * 4 + kk) * FRAG];
-#pragma unroll
-      for (int j = 0; j < LT; ++j) bb[j] = Ys[(j * 4 + kk) * FRAG];
-#pragma unroll
-      for (int i = 0; i < KT; ++i)
-#pragma unroll
-        for (int j = 0; j < LT; ++j) dmma(acc[i][j], a[i], bb[j]);
-    }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      mbar_arrive(&empty[s]);
-      last = (atomicAdd(&relcnt[s], 1u) % 8) == 7;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && b + stages < b1) {
-      mbar_wait(&empty[s], ph);
-      if (lane == 0) packed_issue<NT>(ring + s * STAGE, Xp, Yp, b + stages, hl0, NTH, &full[s], pol, NX);
-      __syncwarp();
-    }
-    if (++s == stages) {
-      s = 0;
-      ph ^= 1;
-    }
-  }
-  // C tile (i, j): rows k = (kt0+i)*8 + lane/4, cols l = (lt0+j)*8 + 2*(lane%4) + e
-#pragma unroll
-  for (int i = 0; i < KT; ++i)
-#pragma unroll
-    for (int j = 0; j < LT; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        slot[(int64_t)((lt0 + j) * 8 + 2 * (lane & 3) + e) * NP + (kt0 + i) * 8 + (lane >> 2)] = acc[i][j][e];
-}
-
-__host__ __device__ constexpr int packed_parts(int NT) { return NT <= 28 ? 2 : 3; }  // output column parts (registers)
-
-template <int NT>
-__global__ void __launch_bounds__(256, 1)
-gram_packed_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp, int nblk, double* __restrict__ P,
-                   int stages) {
-  constexpr int NP = NT * 8;
-  constexpr int NCP = packed_parts(NT);
-  constexpr int NTH0 = (NT + NCP - 1) / NCP;       // l-tiles per column part (the last may have fewer)
-  constexpr int KTW = (NT + 3) / 4;                // max k-tiles per warp (4 warps along k)
-  constexpr int LTW = (NTH0 + 1) / 2;              // max l-tiles per warp (2 warps along l)
-  constexpr int STAGE = (NT + NTH0) * 4 * FRAG;    // doubles per ring stage (X all, Y one part)
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + 8;
-  unsigned* relcnt = reinterpret_cast<unsigned*>(empty + 8);
-  double* ring = reinterpret_cast<double*>(smem + 256);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slice = blockIdx.x, nslices = gridDim.x, half = blockIdx.y;
-  const int b0 = (int)((int64_t)nblk * slice / nslices), b1 = (int)((int64_t)nblk * (slice + 1) / nslices);
-  const int hl0 = half * NTH0, NTH = min(NTH0, NT - hl0);
-  const uint64_t pol = policy_evict_last();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
-      relcnt[s] = 0u;
-    }
-    mbar_fence_init();
-    for (int s = 0; s < stages && b0 + s < b1; ++s)
-      packed_issue<NT>(ring + s * STAGE, Xp, Yp, b0 + s, hl0, NTH, &full[s], pol);
-  }
-  __syncthreads();
-  double* slot = P + (int64_t)slice * NP * NP;
-  const int wk = warp & 3, wl = warp >> 2;
-  const int kt0 = wk * NT / 4, nkt = (wk + 1) * NT / 4 - kt0;          // floor/ceil split
-  const int lt0 = hl0 + wl * NTH / 2, nlt = hl0 + (wl + 1) * NTH / 2 - lt0;
-  // warp-uniform dispatch to a compile-time tile block (no predicated DMMA)
-  if (nkt == KTW && nlt == LTW)
-    packed_gram_body<NT, KTW, LTW>(ring, STAGE, full, empty, relcnt, stages, b0, b1, kt0, lt0, hl0, NTH, Xp, Yp,
-                                   slot, lane, pol);
-  else if (nkt == KTW)
-    packed_gram_body<NT, KTW, LTW - 1>(ring, STAGE, full, empty, relcnt, stages, b0, b1, kt0, lt0, hl0, NTH, Xp,
-                                       Yp, slot, lane, pol);
-  else if (nlt == LTW)
-    packed_gram_body<NT, KTW - 1, LTW>(ring, STAGE, full, empty, relcnt, stages, b0, b1, kt0, lt0, hl0, NTH, Xp,
-                                       Yp, slot, lane, pol);
-  else
-    packed_gram_body<NT, KTW - 1, LTW - 1>(ring, STAGE, full, empty, relcnt, stages, b0, b1, kt0, lt0, hl0, NTH,
-                                           Xp, Yp, slot, lane, pol);
 }
 
 // K4' for a symmetric product (X^T Y, G symmetric in exact arithmetic: the Euclidean Gram Z^T Z
@@ -1080,31 +968,6 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
 }
 
 template <int NT>
-static cudaError_t gram_packed_nt(int64_t m, const double* Xp, const double* Yp, double* P, int* g_out,
-                                  cudaStream_t s) {
-  constexpr int NCP = packed_parts(NT);
-  constexpr int NTH0 = (NT + NCP - 1) / NCP;
-  const size_t stage = (size_t)(NT + NTH0) * 4 * FRAG * 8;
-  int stages = (int)((SMEM_MAX - 256) / stage);
-  if (stages > 8) stages = 8;
-  const size_t bytes = 256 + stages * stage;
-  {
-    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_packed_kernel<NT>), (int)bytes);
-    if (e != cudaSuccess) return e;
-  }
-  const int64_t nblk = zp_blocks(m);
-  int64_t nsl = num_sms() / NCP;
-  if (nsl > nblk) nsl = nblk;
-  *g_out = (int)nsl;
-  timing_begin(s, OQR_TIMING_K4);
-  gram_packed_kernel<NT><<<dim3((unsigned)nsl, NCP), 256, bytes, s>>>(Xp, Yp, (int)nblk, P, stages);
-  note_launch();
-  cudaError_t e = cudaGetLastError();
-  timing_end(s);
-  return e;
-}
-
-template <int NT>
 static cudaError_t gram_packed_upper_nt(int64_t m, const double* Xp, const double* Yp, double* P, int* g_out,
                                         cudaStream_t s) {
   constexpr int NCP = pairs_parts(NT);
@@ -1149,10 +1012,10 @@ cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int
 }
 
 cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
-                               cudaStream_t s, bool upper) {
+                               cudaStream_t s) {
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT) \
-  case NT: return upper ? gram_packed_upper_nt<NT>(m, Xp, Yp, P, g_out, s) : gram_packed_nt<NT>(m, Xp, Yp, P, g_out, s);
+  case NT: return gram_packed_upper_nt<NT>(m, Xp, Yp, P, g_out, s);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

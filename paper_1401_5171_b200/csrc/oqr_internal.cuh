@@ -68,11 +68,11 @@ cudaError_t launch_sum_partials(int n, int count, const double* P, double* G, in
 // Zp and W = T Z (T = tridiag(e, d, e)), both packed, in one pass over Z.
 cudaError_t launch_pack_zw_tridiag(int64_t m, int n, const double* d, const double* e, const double* Z, int64_t ldz,
                                    double* Zp, double* Wp, cudaStream_t s);
-// Slots of X^T Y for two packed m x n operands (X = Y = Zp: the Euclidean Gram).  upper: the
-// product is symmetric (in exact arithmetic) and only its upper triangle is needed -- the slots
-// then hold the upper tiles only (reduce with mirror = true).
+// Slots of the upper triangle of X^T Y for two packed m x n operands whose product is symmetric
+// in exact arithmetic (X = Y = Zp: the Euclidean Gram; Zp and T Z: the tridiagonal one); reduce
+// with mirror = true.
 cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
-                               cudaStream_t s, bool upper = false);
+                               cudaStream_t s);
 // G (n x n, ldg) = sum_{c<g} P[c] in fixed c order.
 cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s,
                                bool sym = false,
