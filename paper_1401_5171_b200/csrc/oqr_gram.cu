@@ -125,7 +125,10 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 // above and below for the stencil) with coalesced column reads, then writes the tile's 4 x 4
 // fragment groups of Zp (and W = T Z) as contiguous 1 KiB runs.  TRI: also W, w_il =
 // e_{i-1} z_{i-1,l} + d_i z_il + e_i z_{i+1,l} (fma order as the per-element kernel).
-constexpr int PT_R = 64, PT_C = 32;
+#ifndef OQR_EXP_PT_C
+#define OQR_EXP_PT_C 32
+#endif
+constexpr int PT_R = 64, PT_C = OQR_EXP_PT_C;
 template <bool TRI>
 __global__ void __launch_bounds__(256)
 pack_tile_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t ldz, double* __restrict__ Zp,
@@ -168,7 +171,7 @@ pack_tile_kernel(int64_t m, int n, int NT, const double* __restrict__ Z, int64_t
     // 4 row blocks x 4 column tiles, 128 doubles each: o -> (block, tile, kk, lane)
     for (int o = threadIdx.x; o < (PT_R / BK) * (PT_C / 8) * 4 * FRAG; o += blockDim.x) {
       const int grp = o >> 7, w = o & 127;
-      const int bl = grp >> 2, tl = grp & 3;
+      const int bl = grp / (PT_C / 8), tl = grp % (PT_C / 8);
       const int kk = w >> 5, ln = w & 31;
       const int r = bl * BK + kk * 4 + (ln & 3);  // tile-local row
       const int c = tl * 8 + (ln >> 2);           // tile-local column
