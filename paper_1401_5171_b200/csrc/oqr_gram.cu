@@ -707,7 +707,7 @@ gram_packed_pairs_kernel(const double* __restrict__ Xp, const double* __restrict
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = blockIdx.x, nslices = gridDim.x;
   const int b0 = (int)((int64_t)nblk * slice / nslices), b1 = (int)((int64_t)nblk * (slice + 1) / nslices);
-  const uint64_t pol = policy_evict_last();
+  const uint64_t pol = policy_evict_first();  // Xp, Yp are streamed once
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
