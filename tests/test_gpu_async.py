@@ -1,11 +1,9 @@
 """Asynchronous, CUDA-graph-capturable entry points (oqr_*_async with a caller workspace and a
 device status word): bitwise the same results as the synchronous calls, breakdown codes delivered
 through d_status, and a captured CUDA graph replayed on fresh inputs."""
-import numpy as np
 import pytest
 
 import gen
-import oracle
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu

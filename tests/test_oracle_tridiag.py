@@ -11,7 +11,7 @@ import pytest
 
 import gen
 import oracle
-from oracle import U, gamma
+from oracle import U
 
 
 def test_spec_stencil_example():
