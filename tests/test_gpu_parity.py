@@ -521,3 +521,24 @@ def test_t1_packed_upper_gram_part_boundaries(oqr, n):
     Td = np.abs(np.diag(d)) + np.abs(np.diag(e, 1)) + np.abs(np.diag(e, -1))
     Mt = np.abs(Zd).T @ (Td @ np.abs(Zd))
     assert np.all(np.abs(Gt - Got) <= 2 * gamma(m + 3) * Mt)
+
+
+def test_timing_hook_per_kernel(oqr):
+    """oqr_timing_read_kernel: one K1, K2, K3 launch per oqr_normal; prequr adds the packed Gram
+    (K4') and a second K2/K3; the K1 reading equals oqr_timing_read's."""
+    p = make(2000, 30, 1e2, 1e2, 81)
+    A, Z = to_dev(p.A), to_dev(p.Z)
+    oqr.timing_enable(True)
+    try:
+        oqr.timing_reset()
+        oqr.normal(A, Z)
+        counts = {k: oqr.timing_read_kernel(k)[1] for k in ("K1", "K4", "K3", "K2")}
+        assert counts == {"K1": 1, "K4": 0, "K3": 1, "K2": 1}, counts
+        ms, k1, _ = oqr.timing_read()
+        assert k1 == 1 and ms == oqr.timing_read_kernel("K1")[0] and ms > 0
+        oqr.timing_reset()
+        oqr.prequr(A, Z)
+        counts = {k: oqr.timing_read_kernel(k)[1] for k in ("K1", "K4", "K3", "K2")}
+        assert counts == {"K1": 1, "K4": 1, "K3": 2, "K2": 2}, counts
+    finally:
+        oqr.timing_enable(False)
