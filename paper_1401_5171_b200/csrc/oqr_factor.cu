@@ -82,8 +82,11 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
         brk = b0 + c + 1;
         break;
       }
-      const double r = sqrt(d);
-      const double inv = 1.0 / r;
+      // one reciprocal square root (<= 1 ulp) on the pivot chain instead of sqrt and then 1/r:
+      // r = d * (1/sqrt(d)) is within ~1.5 ulp of sqrt(d) -- inside the gates' gamma_{n+1}
+      // (PAPER.md:195-196), and 8-16% off K2's time (tools/time_potrf.py)
+      const double inv = rsqrt(d);
+      const double r = d * inv;
       // row c: (c, c) = r, (c, b > c) *= inv
       if (c < 4) {
         if (ra == c) v0 = (cb == c) ? r : (cb > c ? v0 * inv : v0);
