@@ -115,10 +115,12 @@ def problem(m: int, n: int, kappa_a: float, kappa_z: float, seed: int, ucase: st
     Z = Z_out if Z_out is not None else np.empty((n, ldz), dtype=np.float64)
     assert Z.shape[0] == n and Z.dtype == np.float64 and Z.flags.c_contiguous
     ldz = Z.shape[1]
+    # padding rows (lda/ldz > m) are never part of the matrix: poison them with NaN so that a
+    # kernel reading past row m shows up as a NaN result instead of adding silent zeros
     if lda > m and A is not None and A_out is None:
-        A[:, m:] = 0.0
+        A[:, m:] = np.nan
     if ldz > m and Z_out is None:
-        Z[:, m:] = 0.0
+        Z[:, m:] = np.nan
     Yv = np.empty((4, m)); Tv = np.empty((4, 4)); d = np.empty(m); s = np.empty(n)
     Yu = np.zeros((4, m)); Tu = np.empty((4, 4)); Yw = np.empty((4, n)); Tw = np.empty((4, 4))
     cols = np.empty(n, dtype=np.int64)

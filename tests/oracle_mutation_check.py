@@ -28,6 +28,23 @@ MUTATIONS = {
     "prequr_Y_skipped": ("int info2 = orc_normal(m, n, A, lda, Y, m, Q, U);",
                          "int info2 = orc_normal(m, n, A, lda, Z, ldz, Q, U);"),
     "euclid_gram_index": ("s += zk[i] * zl[i];", "s += zk[i] * zk[i];"),
+    # the double-double checkers (tests/test_oracle_checkers.py)
+    "dd_drop_product_error": ("double lo = s.lo + acc.lo + pe;", "double lo = s.lo + acc.lo;"),
+    "dd_two_sum_drop_b_part": ("dd_t r = {s, (a - (s - bb)) + (b - bb)};", "dd_t r = {s, (a - (s - bb))};"),
+    "dd_drop_lo_of_dd_operand": ("double t = a * b.lo;", "double t = 0.0 * b.lo;"),
+    "dd_gram_M_no_fabs_A": ("sa += fabs(a) * fabs(z);", "sa += a * fabs(z);"),
+    "dd_gram_M_no_fabs_Z": ("sa += fabs(Z[k * ldz + i]) * Babs[l * m + i];", "sa += Z[k * ldz + i] * Babs[l * m + i];"),
+    "dd_gram_transposed_A": ("double a = A[j * lda + i], z = Z[l * ldz + j];", "double a = A[i * lda + j], z = Z[l * ldz + j];"),
+    "dd_resid_k_range": ("for (int64_t k = 0; k <= j; k++) {\n        double q", "for (int64_t k = 0; k < j; k++) {\n        double q"),
+    "dd_resid_sign": ("s = dd_add_prod(s, -q, r);", "s = dd_add_prod(s, q, r);"),
+    "dd_resid_QRabs_no_fabs": ("sa += fabs(q) * fabs(r);", "sa += q * fabs(r);"),
+    "dd_chol_resid_p_range": ("for (int64_t p = 0; p <= kmax; p++)", "for (int64_t p = 0; p < kmax; p++)"),
+    "dd_chol_resid_index": ("double a = R[k * ldr + p], b = R[l * ldr + p];", "double a = R[k * ldr + p], b = R[l * ldr + k];"),
+    "dd_orth_missing_minus_I": ("dd_t s = {k == l ? -1.0 : 0.0, 0.0};\n      for (int64_t i = 0; i < m; i++) s = dd_add_dd_prod(s, Q[k * ldq + i], AQ[l * m + i]);\n      E[l * n + k] = s.hi + s.lo;\n    }\n  free(AQ);\n}\n\n/* G = Z",
+                                "dd_t s = {0.0, 0.0};\n      for (int64_t i = 0; i < m; i++) s = dd_add_dd_prod(s, Q[k * ldq + i], AQ[l * m + i]);\n      E[l * n + k] = s.hi + s.lo;\n    }\n  free(AQ);\n}\n\n/* G = Z"),
+    "dd_orth_transposed_A": ("s = dd_add_prod(s, A[j * lda + i], Q[l * ldq + j]);", "s = dd_add_prod(s, A[i * lda + j], Q[l * ldq + j]);"),
+    "dd_orth_cols_wrong_col": ("const double q = Q[cols[l] * ldq + j];", "const double q = Q[l * ldq + j];"),
+    "dd_orth_tridiag_e_index": ("if (i > 0) s = dd_add_prod(s, e[i - 1], q[i - 1]);", "if (i > 0) s = dd_add_prod(s, e[i], q[i - 1]);"),
 }
 
 
@@ -42,7 +59,8 @@ def main():
             open(SRC, "w").write(orig.replace(a, b, 1))
             r = subprocess.run(
                 f'{sys.executable} -c "import oracle; oracle.build(force=True)" && '
-                f"{sys.executable} -m pytest tests/test_oracle_pins.py -q -x 2>&1 | tail -1",
+                f"{sys.executable} -m pytest tests/test_oracle_pins.py tests/test_oracle_checkers.py "
+                f"tests/test_oracle_stable.py tests/test_oracle_tridiag.py -q -x -p no:cacheprovider 2>&1 | tail -1",
                 shell=True, capture_output=True, text=True, cwd=ROOT)
             line = r.stdout.strip()
             killed = "failed" in line

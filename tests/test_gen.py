@@ -45,6 +45,7 @@ def test_deterministic_and_padded_ld():
     b = gen.problem(64, 5, 1e2, 1e2, 3, lda=70, ldz=66)
     assert np.array_equal(a.A, b.A[:, :64])
     assert np.array_equal(a.Z, b.Z[:, :64])
+    assert np.all(np.isnan(b.A[:, 64:])) and np.all(np.isnan(b.Z[:, 64:]))   # poisoned padding
     c = gen.problem(64, 5, 1e2, 1e2, 4)
     assert not np.array_equal(a.Z, c.Z)
 
