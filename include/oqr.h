@@ -161,6 +161,25 @@ int oqr_prequr_stable_tridiag(int64_t m, int64_t n, const double* d, const doubl
                               int64_t ldz, double* Q, double* R, oqr_stream_t stream);
 
 /*
+ * oqr_prequr_hh -- PRE-CHOLQR exactly as Algorithm 2 states it: the pre-step
+ * [Y, S] = qr(Z) is a Householder QR, "a stable Euclidean QR factorization (such as Householder
+ * QR)", the pre-step Theorem 3 is proved for; then
+ * [Q, U] = CHOLQR(A, Y) and R = U S.  The pre-step is backward stable for EVERY
+ * full-rank Z (no kappa(Z) limit: ||Y^T Y - I|| = O(m n u), ||Z - Y S|| = O(m n u) ||Z||) and never
+ * breaks down; only the A-stage can (status n + k).  S has a positive diagonal (LAPACK dlarfg
+ * reflectors, then row/column sign flips, exact).  Y lives in Q.  Householder QR runs as one
+ * cooperative kernel (all CTAs co-resident, grid barriers) whose per-CTA row block must fit in
+ * shared memory: m up to ~1.5e5 at n = 240 (larger m: status -1).
+ * _sym / _tridiag: the same with the symmetric (block-lower) or tridiagonal A-stage.
+ */
+int oqr_prequr_hh(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                  double* Q, double* R, oqr_stream_t stream);
+int oqr_prequr_hh_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                      double* Q, double* R, oqr_stream_t stream);
+int oqr_prequr_hh_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z,
+                          int64_t ldz, double* Q, double* R, oqr_stream_t stream);
+
+/*
  * Asynchronous variants (CUDA-graph capturable).  Same computation as the synchronous calls, but
  * nothing is synchronised: the call enqueues its kernels on `stream` and returns 0 (or a negative
  * argument status, nothing enqueued); the factorisation status (0, k, n + k as above) is written to
@@ -179,6 +198,9 @@ int oqr_prequr_async(int64_t m, int64_t n, const double* A, int64_t lda, const d
 int oqr_prequr_stable_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                             double* Q, double* R, void* workspace, size_t workspace_bytes, int* d_status,
                             oqr_stream_t stream);
+int oqr_prequr_hh_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                        double* Q, double* R, void* workspace, size_t workspace_bytes, int* d_status,
+                        oqr_stream_t stream);
 
 /* Human-readable text for a status code (static storage; never NULL). */
 const char* oqr_status_string(int status);
@@ -212,6 +234,12 @@ int oqr_potrf(int64_t n, const double* G, double* R, int* d_info, oqr_stream_t s
 int oqr_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, double* Q,
              oqr_stream_t stream);
 
+/* [Y, S] = Householder QR of Z (Algorithm 2 line 1; the pre-step of oqr_prequr_hh):
+ * Y m x n (ld m) with orthonormal columns, S n x n (ld n) upper triangular with positive diagonal,
+ * Z = Y S.  Y must not overlap Z.  Asynchronous.  Status 0, -1 m (too large, see oqr_prequr_hh),
+ * -2 n, -5 Z, -6 ldz, -7 Y, -8 S, -100 CUDA, -101 workspace. */
+int oqr_hhqr(int64_t m, int64_t n, const double* Z, int64_t ldz, double* Y, double* S, oqr_stream_t stream);
+
 /* ---- Row-sharded multi-GPU path.  Rank r holds rows
  *      R_r = [r0, r0 + mr) of A and all of Z.  Because G = sum_r Z_{R_r}^T (A_{R_r,:} Z) for any
  *      partition of the rows (bilinearity of Algorithm 1 lines 1-2), each rank
@@ -239,11 +267,13 @@ void oqr_timing_reset(void);
 int oqr_timing_read(double* gram_ms, int64_t* gram_launches, int64_t* total_launches);
 /* The same hook for one kernel family: OQR_TIMING_K1 (fused Gram, as oqr_timing_read),
  * OQR_TIMING_K4 (packed tall-skinny Gram: Euclidean / tridiagonal), OQR_TIMING_K3 (triangular
- * solve), OQR_TIMING_K2 (Cholesky).  Status 0, -1 unknown kernel, -100 CUDA. */
+ * solve), OQR_TIMING_K2 (Cholesky), OQR_TIMING_K6 (Householder QR).  Status 0, -1 unknown kernel,
+ * -100 CUDA. */
 #define OQR_TIMING_K1 0
 #define OQR_TIMING_K4 1
 #define OQR_TIMING_K3 2
 #define OQR_TIMING_K2 3
+#define OQR_TIMING_K6 4
 int oqr_timing_read_kernel(int kernel, double* ms, int64_t* launches);
 
 /* Number of kernels this library has launched since load (all entry points). */

@@ -68,6 +68,11 @@ def _load():
             "orc_normal2_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
             "orc_prequr_tridiag": (ctypes.c_int, [I, I, P, P, P, I, P, P]),
             "orc_dd_orth_tridiag": (None, [I, I, P, P, P, I, P]),
+            "orc_geqr2": (None, [I, I, P, I, P]),
+            "orc_org2r": (None, [I, I, P, I, P, P]),
+            "orc_hhqr": (ctypes.c_int, [I, I, P, I, P, P]),
+            "orc_prequr_hh": (ctypes.c_int, [I, I, P, I, P, I, P, P]),
+            "orc_dd_orth_euclid": (None, [I, I, P, I, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -187,7 +192,51 @@ def scqr3(Z, m):
     return Y, S, info
 
 
-VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr, "prequr_stable": prequr_stable}
+def prequr_hh(A, Z, m):
+    """PRE-CHOLQR exactly as Algorithm 2 states it: Householder QR pre-step
+    (NEXT-N1, paper-faithful), then CHOLQR(A, Y) and R = U S."""
+    return _variant("orc_prequr_hh", A, Z, m)
+
+
+def hhqr(Z, m):
+    """Householder QR of Z with positive-diagonal S: (Y storage (n, m), S storage (n, n))."""
+    Z, ldz = _cm(Z, m)
+    n = Z.shape[0]
+    Y = np.zeros((n, m))
+    S = np.zeros((n, n))
+    _load().orc_hhqr(m, n, _p(Z), ldz, _p(Y), _p(S))
+    return Y, S
+
+
+def geqr2(Z, m):
+    """LAPACK-convention unblocked Householder QR: (X storage (n, m) with R on/above and the
+    reflector vectors below the diagonal, tau (n,))."""
+    X, ldx = _cm(np.array(Z, dtype=np.float64, copy=True), m)
+    n = X.shape[0]
+    tau = np.zeros(n)
+    _load().orc_geqr2(m, n, _p(X), ldx, _p(tau))
+    return X, tau
+
+
+def orth_error_euclid(Y, m) -> float:
+    """||Y^T Y - I||_2, check formed in double-double."""
+    Y, ldy = _cm(Y, m)
+    n = Y.shape[0]
+    E = np.empty((n, n))
+    _load().orc_dd_orth_euclid(m, n, _p(Y), ldy, _p(E))
+    return float(np.linalg.norm(E.T, 2))
+
+
+def dd_orth_euclid_matrix(Y, m) -> np.ndarray:
+    Y, ldy = _cm(Y, m)
+    n = Y.shape[0]
+    E = np.empty((n, n))
+    _load().orc_dd_orth_euclid(m, n, _p(Y), ldy, _p(E))
+    return E.T.copy()
+
+
+VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr, "prequr_stable": prequr_stable,
+            "prequr_hh": prequr_hh}
 
 
 # -------------------------------------------------------------- checkers ---

@@ -531,3 +531,104 @@ int orc_prequr_stable(int64_t m, int64_t n, const double* A, int64_t lda, const 
   free(S); free(U); free(Y);
   return info;
 }
+
+/* ========================================================================= */
+/* NEXT-N1 (paper-faithful): PRE-CHOLQR with a Householder Euclidean pre-step. */
+/* Algorithm 2 line 1: "[Y,S] = qr(Z)" with "a stable       */
+/* Euclidean QR factorization (such as Householder QR)".    */
+/* Plain unblocked Householder QR (LAPACK dgeqr2 / dlarfg convention) and the  */
+/* explicit first n columns of Q (dorg2r: reflectors applied to I[:, :n] in    */
+/* reverse order), then the positive-diagonal normalisation of the problem     */
+/* statement (R with positive diagonal): for r_jj < 0 the row  */
+/* j of S and the column j of Y change sign (exact).                           */
+/*   column j:  alpha = X[j,j];  nrm2 = sum_{i>=j} X[i,j]^2 (i ascending);     */
+/*     if nrm2 == alpha^2 (x below the diagonal is zero): tau_j = 0, beta = alpha */
+/*     else beta = -sign(alpha) sqrt(nrm2);  tau_j = (beta - alpha) / beta;    */
+/*          v_j = 1, v_i = X[i,j] / (alpha - beta) (i > j);  X[j,j] = beta;    */
+/*     for l > j:  w = X[j,l] + sum_{i>j} v_i X[i,l];  X[i,l] -= tau_j v_i w.  */
+/* ========================================================================= */
+void orc_geqr2(int64_t m, int64_t n, double* X, int64_t ldx, double* tau) {
+  for (int64_t j = 0; j < n; j++) {
+    double* xj = X + j * ldx;
+    const double alpha = xj[j];
+    double tail = 0.0;
+    for (int64_t i = j + 1; i < m; i++) tail += xj[i] * xj[i];
+    if (tail == 0.0) { tau[j] = 0.0; continue; }
+    const double nrm = sqrt(alpha * alpha + tail);
+    const double beta = alpha >= 0.0 ? -nrm : nrm;
+    tau[j] = (beta - alpha) / beta;
+    const double scal = 1.0 / (alpha - beta);
+    for (int64_t i = j + 1; i < m; i++) xj[i] *= scal;
+    xj[j] = beta;
+    for (int64_t l = j + 1; l < n; l++) {
+      double* xl = X + l * ldx;
+      double w = xl[j];
+      for (int64_t i = j + 1; i < m; i++) w += xj[i] * xl[i];
+      xl[j] -= tau[j] * w;
+      for (int64_t i = j + 1; i < m; i++) xl[i] -= tau[j] * xj[i] * w;
+    }
+  }
+}
+
+/* Y (m x n, ld m) = H_0 H_1 ... H_{n-1} I[:, :n] with H_j = I - tau_j v_j v_j^T (v_j stored
+ * below the diagonal of X, unit at j): the reflectors applied to I[:, :n] last to first. */
+void orc_org2r(int64_t m, int64_t n, const double* X, int64_t ldx, const double* tau, double* Y) {
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t i = 0; i < m; i++) Y[l * m + i] = (i == l) ? 1.0 : 0.0;
+  for (int64_t j = n - 1; j >= 0; j--) {
+    const double* v = X + j * ldx;
+    for (int64_t l = j; l < n; l++) {
+      double* y = Y + l * m;
+      double w = y[j];
+      for (int64_t i = j + 1; i < m; i++) w += v[i] * y[i];
+      y[j] -= tau[j] * w;
+      for (int64_t i = j + 1; i < m; i++) y[i] -= tau[j] * v[i] * w;
+    }
+  }
+}
+
+/* [Y, S] = Householder QR of Z with positive-diagonal S (Y: m x n ld m, S: n x n ld n). */
+int orc_hhqr(int64_t m, int64_t n, const double* Z, int64_t ldz, double* Y, double* S) {
+  double* X = (double*)malloc(sizeof(double) * m * n);
+  double* tau = (double*)malloc(sizeof(double) * n);
+  for (int64_t l = 0; l < n; l++) memcpy(X + l * m, Z + l * ldz, sizeof(double) * m);
+  orc_geqr2(m, n, X, m, tau);
+  orc_org2r(m, n, X, m, tau, Y);
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) S[l * n + k] = (k <= l) ? X[l * m + k] : 0.0;
+  for (int64_t j = 0; j < n; j++)
+    if (S[j * n + j] < 0.0) {
+      for (int64_t l = j; l < n; l++) S[l * n + j] = -S[l * n + j];
+      for (int64_t i = 0; i < m; i++) Y[j * m + i] = -Y[j * m + i];
+    }
+  free(X); free(tau);
+  return 0;
+}
+
+/* PRE-CHOLQR (Algorithm 2) exactly as the paper states it: Householder pre-step, then
+ * [Q, U] = CHOLQR(A, Y) and R = U S.  A-stage breakdown -> n + k. */
+int orc_prequr_hh(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                  double* Q, double* R) {
+  double* S = (double*)malloc(sizeof(double) * n * n);
+  double* U = (double*)malloc(sizeof(double) * n * n);
+  double* Y = (double*)malloc(sizeof(double) * m * n);
+  int info = orc_hhqr(m, n, Z, ldz, Y, S);
+  if (!info) {
+    int info2 = orc_normal(m, n, A, lda, Y, m, Q, U);
+    if (info2) info = (int)n + info2;
+    else orc_trmm(n, U, n, S, n, R, n);
+  }
+  free(S); free(U); free(Y);
+  return info;
+}
+
+/* E = Y^T Y - I (n x n, ld n), double-double (Euclidean orthogonality of a pre-step factor). */
+void orc_dd_orth_euclid(int64_t m, int64_t n, const double* Y, int64_t ldy, double* E) {
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t l = 0; l < n; l++)
+    for (int64_t k = 0; k < n; k++) {
+      dd_t s = {k == l ? -1.0 : 0.0, 0.0};
+      for (int64_t i = 0; i < m; i++) s = dd_add_prod(s, Y[k * ldy + i], Y[l * ldy + i]);
+      E[l * n + k] = s.hi + s.lo;
+    }
+}

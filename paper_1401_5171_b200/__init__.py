@@ -26,6 +26,7 @@ __all__ = ["normal", "normal2", "prequr", "gram", "gram_euclid", "potrf", "trsm"
 # Every symbol include/oqr.h declares.
 EXPORTS = ("oqr_normal", "oqr_normal_host", "oqr_normal2", "oqr_prequr", "oqr_workspace_bytes", "oqr_normal_async",
            "oqr_normal2_async", "oqr_prequr_async", "oqr_prequr_stable_async", "oqr_prequr_stable", "oqr_prequr_stable_sym",
+           "oqr_prequr_hh", "oqr_prequr_hh_sym", "oqr_prequr_hh_tridiag", "oqr_prequr_hh_async", "oqr_hhqr",
            "oqr_prequr_stable_tridiag", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
            "oqr_gram_sym", "oqr_upload_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
@@ -53,11 +54,13 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(LIB_PATH)
         I64, P, I = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
         for name in ("oqr_normal", "oqr_normal2", "oqr_prequr", "oqr_normal_sym", "oqr_normal2_sym",
-                     "oqr_prequr_sym", "oqr_prequr_stable", "oqr_prequr_stable_sym"):
+                     "oqr_prequr_sym", "oqr_prequr_stable", "oqr_prequr_stable_sym", "oqr_prequr_hh",
+                     "oqr_prequr_hh_sym"):
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, I64, P, I64, P, P, P]
-        for name in ("oqr_normal_tridiag", "oqr_normal2_tridiag", "oqr_prequr_tridiag", "oqr_prequr_stable_tridiag"):
+        for name in ("oqr_normal_tridiag", "oqr_normal2_tridiag", "oqr_prequr_tridiag", "oqr_prequr_stable_tridiag",
+                     "oqr_prequr_hh_tridiag"):
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, P, P, I64, P, P, P]
@@ -67,7 +70,8 @@ def lib() -> ctypes.CDLL:
         L.oqr_status_string.argtypes = [I]
         L.oqr_workspace_bytes.restype = ctypes.c_size_t
         L.oqr_workspace_bytes.argtypes = [I64, I64]
-        for name in ("oqr_normal_async", "oqr_normal2_async", "oqr_prequr_async", "oqr_prequr_stable_async"):
+        for name in ("oqr_normal_async", "oqr_normal2_async", "oqr_prequr_async", "oqr_prequr_stable_async",
+                     "oqr_prequr_hh_async"):
             f = getattr(L, name)
             f.restype = I
             f.argtypes = [I64, I64, P, I64, P, I64, P, P, P, ctypes.c_size_t, P, P]
@@ -85,6 +89,8 @@ def lib() -> ctypes.CDLL:
         L.oqr_potrf.argtypes = [I64, P, P, P, P]
         L.oqr_trsm.restype = I
         L.oqr_trsm.argtypes = [I64, I64, P, I64, P, P, P]
+        L.oqr_hhqr.restype = I
+        L.oqr_hhqr.argtypes = [I64, I64, P, I64, P, P, P]
         L.oqr_gram_rows.restype = I
         L.oqr_gram_rows.argtypes = [I64, I64, I64, I64, P, I64, P, I64, P, P]
         L.oqr_sum_partials.restype = I
@@ -198,7 +204,13 @@ def prequr_stable(A, Z, Q=None, R=None, stream=None, check: bool = True):
     return _variant("oqr_prequr_stable", A, Z, Q, R, stream, check)
 
 
-VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr, "prequr_stable": prequr_stable}
+def prequr_hh(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    """PRE-CHOLQR exactly as Algorithm 2 states it: Householder QR pre-step (NEXT-N1, paper-faithful)."""
+    return _variant("oqr_prequr_hh", A, Z, Q, R, stream, check)
+
+
+VARIANTS = {"normal": normal, "normal2": normal2, "prequr": prequr, "prequr_stable": prequr_stable,
+            "prequr_hh": prequr_hh}
 
 
 def normal_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
@@ -218,7 +230,12 @@ def prequr_stable_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
     return _variant("oqr_prequr_stable_sym", A, Z, Q, R, stream, check)
 
 
-VARIANTS_SYM = {"normal": normal_sym, "normal2": normal2_sym, "prequr": prequr_sym, "prequr_stable": prequr_stable_sym}
+def prequr_hh_sym(A, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant("oqr_prequr_hh_sym", A, Z, Q, R, stream, check)
+
+
+VARIANTS_SYM = {"normal": normal_sym, "normal2": normal2_sym, "prequr": prequr_sym, "prequr_stable": prequr_stable_sym,
+                "prequr_hh": prequr_hh_sym}
 
 
 def upload_sym(A_host, A_dev, stream=None):
@@ -288,8 +305,12 @@ def prequr_stable_tridiag(d, e, Z, Q=None, R=None, stream=None, check: bool = Tr
     return _variant_tridiag("oqr_prequr_stable_tridiag", d, e, Z, Q, R, stream, check)
 
 
+def prequr_hh_tridiag(d, e, Z, Q=None, R=None, stream=None, check: bool = True):
+    return _variant_tridiag("oqr_prequr_hh_tridiag", d, e, Z, Q, R, stream, check)
+
+
 VARIANTS_TRIDIAG = {"normal": normal_tridiag, "normal2": normal2_tridiag, "prequr": prequr_tridiag,
-                    "prequr_stable": prequr_stable_tridiag}
+                    "prequr_stable": prequr_stable_tridiag, "prequr_hh": prequr_hh_tridiag}
 
 
 def gram_tridiag(d, e, Z, G=None, stream=None):
@@ -358,6 +379,21 @@ def trsm(Z, R, m: int | None = None, Q=None, stream=None):
     if st:
         raise OqrError(st, "oqr_trsm")
     return Q
+
+
+def hhqr(Z, m: int | None = None, Y=None, S=None, stream=None):
+    """[Y, S] = Householder QR of Z, positive-diagonal S (asynchronous step export of K6)."""
+    import torch
+    n = Z.shape[0]
+    m = Z.shape[1] if m is None else m
+    if Y is None:
+        Y = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+    if S is None:
+        S = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    st = lib().oqr_hhqr(m, n, _check(Z, "Z", m), Z.shape[1], _check(Y, "Y", m), _check(S, "S", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_hhqr")
+    return Y, S
 
 
 def gram_rows(Ar, Z, r0: int, mr: int, G=None, stream=None):
@@ -436,8 +472,12 @@ def prequr_stable_async(A, Z, Q, R, workspace, status, stream=None):
     _async("oqr_prequr_stable_async", A, Z, Q, R, workspace, status, stream)
 
 
+def prequr_hh_async(A, Z, Q, R, workspace, status, stream=None):
+    _async("oqr_prequr_hh_async", A, Z, Q, R, workspace, status, stream)
+
+
 VARIANTS_ASYNC = {"normal": normal_async, "normal2": normal2_async, "prequr": prequr_async,
-                  "prequr_stable": prequr_stable_async}
+                  "prequr_stable": prequr_stable_async, "prequr_hh": prequr_hh_async}
 
 
 def timing_enable(on: bool = True):
@@ -448,7 +488,7 @@ def timing_reset():
     lib().oqr_timing_reset()
 
 
-TIMING_KERNELS = {"K1": 0, "K4": 1, "K3": 2, "K2": 3}
+TIMING_KERNELS = {"K1": 0, "K4": 1, "K3": 2, "K2": 3, "K6": 4}
 
 
 def timing_read_kernel(kernel: str) -> tuple[float, int]:

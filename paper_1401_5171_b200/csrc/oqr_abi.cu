@@ -91,14 +91,16 @@ struct Workspace {
   double* R2 = nullptr;    // n x n (R2 of normal2 / U of prequr)
   double* R3 = nullptr;    // n x n (stable pre-step: R2, R3 of the CholeskyQR2 stage)
   double* R4 = nullptr;    // n x n (stable pre-step: products)
+  double* H = nullptr;     // Householder QR scratch (K6): hh_scratch_doubles(m, n)
   int* info = nullptr;
   cudaStream_t s = nullptr;
+  static size_t hh_doubles(int64_t m, int n) { return 2 * cdiv((int64_t)hh_scratch_doubles(m, n), 2); }
   static size_t doubles_for(int64_t m, int n, int64_t mr_local) {
     const int NP = 8 * (int)cdiv(n, 8);
     const size_t zp = (size_t)zp_doubles(m, NP);
     const size_t zc = mr_local > 0 ? (size_t)zp_doubles(mr_local, NP) : 0;
     const size_t sl = slots_doubles(n, gram_grid(m));
-    return zp + zc + sl + 5 * (size_t)n * n + 2;  // +2 doubles (16 B) for info
+    return zp + zc + sl + 5 * (size_t)n * n + 1 + hh_doubles(m, n) + 2;  // +1 pad, +2 doubles (16 B) for info
   }
   // user_ws: caller-provided workspace of user_bytes (no allocation: CUDA-graph capturable);
   // user_info: device status word to use instead of the workspace's own.
@@ -133,7 +135,8 @@ struct Workspace {
     R2 = R1 + nn;
     R3 = R2 + nn;
     R4 = R3 + nn;
-    info = user_info ? user_info : reinterpret_cast<int*>(R4 + nn);
+    H = R4 + nn + ((nn & 1) ? 1 : 0);  // 16-byte aligned
+    info = user_info ? user_info : reinterpret_cast<int*>(H + hh_doubles(m, n));
     return 0;
   }
   ~Workspace() {
@@ -383,6 +386,22 @@ static int run_prequr_stable(const AOp& op, int64_t m, int n, const double* Z, i
   return as ? 0 : finish(ws, s);
 }
 
+// PRE-CHOLQR as Algorithm 2 states it (NEXT-N1, paper-faithful): Householder QR pre-step (K6):
+//   [Y, S] = qr(Z) (Y into Q, S into R1);  [Q, U] = CHOLQR(A, Y) in place (U into R2);  R = U S.
+static int run_prequr_hh(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
+                         cudaStream_t s, const Async* as = nullptr) {
+  if (!hh_supported(m, n)) return -1;
+  Workspace ws;
+  int st = as ? ws.alloc(m, n, s, m, as->ws, as->bytes, as->d_status)
+              : ws.alloc(m, n, s, (op.tridiag || op.sym) ? m : 0);
+  if (st) return st;
+  OQR_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), s));  // the pre-step never breaks down
+  OQR_TRY(launch_hhqr(m, n, Z, ldz, ws.Zp, Q, ws.R1, ws.H, s));
+  if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
+  if ((st = cuda_status(launch_trmm(n, ws.R2, ws.R1, R, ws.info, s)))) return st;   // R = U S
+  return as ? 0 : finish(ws, s);
+}
+
 static AOp dense_op(const double* A, int64_t lda, bool sym = false) {
   AOp op;
   op.A = A;
@@ -467,6 +486,7 @@ static int async_call(int which, int64_t m, int64_t n, const double* A, int64_t 
     case 0: return run_normal(op, m, (int)n, Z, ldz, Q, R, s, &as);
     case 1: return run_normal2(op, m, (int)n, Z, ldz, Q, R, s, &as);
     case 2: return run_prequr(op, m, (int)n, Z, ldz, Q, R, s, &as);
+    case 4: return run_prequr_hh(op, m, (int)n, Z, ldz, Q, R, s, &as);
     default: return run_prequr_stable(op, m, (int)n, Z, ldz, Q, R, s, &as);
   }
 }
@@ -490,6 +510,43 @@ int oqr_prequr_stable_async(int64_t m, int64_t n, const double* A, int64_t lda, 
                             double* Q, double* R, void* workspace, size_t workspace_bytes, int* d_status,
                             oqr_stream_t stream) {
   return async_call(3, m, n, A, lda, Z, ldz, Q, R, workspace, workspace_bytes, d_status, stream);
+}
+
+int oqr_prequr_hh_async(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                        double* Q, double* R, void* workspace, size_t workspace_bytes, int* d_status,
+                        oqr_stream_t stream) {
+  return async_call(4, m, n, A, lda, Z, ldz, Q, R, workspace, workspace_bytes, d_status, stream);
+}
+
+int oqr_prequr_hh(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                  double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  return run_prequr_hh(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_prequr_hh_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
+                      double* Q, double* R, oqr_stream_t stream) {
+  int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
+  if (st) return st;
+  return run_prequr_hh(dense_op(A, lda, true), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_prequr_hh_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
+                          double* Q, double* R, oqr_stream_t stream) {
+  int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
+  if (st) return st;
+  return run_prequr_hh(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int oqr_hhqr(int64_t m, int64_t n, const double* Z, int64_t ldz, double* Y, double* S, oqr_stream_t stream) {
+  int st = check_args(m, n, nullptr, m, Z, ldz, Y, S, false, true);
+  if (st) return st;
+  if (!hh_supported(m, (int)n)) return -1;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws;
+  if ((st = ws.alloc(m, (int)n, s))) return st;
+  return cuda_status(launch_hhqr(m, (int)n, Z, ldz, ws.Zp, Y, S, ws.H, s));
 }
 
 int oqr_prequr_stable(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
@@ -687,7 +744,7 @@ void oqr_timing_reset(void) {
 }
 
 int oqr_timing_read_kernel(int kernel, double* ms_out, int64_t* launches) {
-  if (kernel < 0 || kernel > 3) return -1;
+  if (kernel < 0 || kernel > 4) return -1;
   double ms = 0.0;
   int64_t k = 0;
   for (size_t i = 0; i < g_event_used; ++i) {

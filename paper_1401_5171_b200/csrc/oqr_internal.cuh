@@ -90,6 +90,14 @@ cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const do
 cudaError_t launch_trmm(int n, const double* R2, const double* R1, double* R, const int* info,
                         cudaStream_t s);
 
+// K6: Householder QR of Z (m x n, ldz) -> Y (m x n, ld m), S (n x n, ld n, positive diagonal);
+// X: m x n working matrix (ld m); scratch: hh_scratch_doubles(m, n) doubles, 16-byte aligned.
+// One cooperative launch (grid barriers).  hh_supported: the per-CTA row block fits in shared memory.
+cudaError_t launch_hhqr(int64_t m, int n, const double* Z, int64_t ldz, double* X, double* Y, double* S,
+                        double* scratch, cudaStream_t s);
+size_t hh_scratch_doubles(int64_t m, int n);
+bool hh_supported(int64_t m, int n);
+
 // Workspace size (bytes) for the Gram of an (m, n) problem on a grid of g CTAs.
 int gram_grid(int64_t m);
 size_t slots_doubles(int n, int g);

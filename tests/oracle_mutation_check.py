@@ -44,6 +44,21 @@ MUTATIONS = {
                                 "dd_t s = {0.0, 0.0};\n      for (int64_t i = 0; i < m; i++) s = dd_add_dd_prod(s, Q[k * ldq + i], AQ[l * m + i]);\n      E[l * n + k] = s.hi + s.lo;\n    }\n  free(AQ);\n}\n\n/* G = Z"),
     "dd_orth_transposed_A": ("s = dd_add_prod(s, A[j * lda + i], Q[l * ldq + j]);", "s = dd_add_prod(s, A[i * lda + j], Q[l * ldq + j]);"),
     "dd_orth_cols_wrong_col": ("const double q = Q[cols[l] * ldq + j];", "const double q = Q[l * ldq + j];"),
+    # the Householder pre-step (tests/test_oracle_hh.py)
+    "hh_beta_sign": ("const double beta = alpha >= 0.0 ? -nrm : nrm;", "const double beta = alpha >= 0.0 ? nrm : -nrm;"),
+    "hh_tau": ("tau[j] = (beta - alpha) / beta;", "tau[j] = (beta - alpha) / alpha;"),
+    "hh_tail_from_diag": ("for (int64_t i = j + 1; i < m; i++) tail += xj[i] * xj[i];",
+                          "for (int64_t i = j + 2; i < m; i++) tail += xj[i] * xj[i];"),
+    "hh_update_drop_diag_term": ("double w = xl[j];\n      for", "double w = 0.0;\n      for"),
+    "hh_org2r_forward_order": ("for (int64_t j = n - 1; j >= 0; j--) {\n    const double* v = X + j * ldx;",
+                               "for (int64_t jj = 0; jj < n; jj++) {\n    const int64_t j = jj;\n    const double* v = X + j * ldx;"),
+    "hh_org2r_cols_from_0": ("for (int64_t l = j; l < n; l++) {\n      double* y = Y + l * m;",
+                             "for (int64_t l = j + 1; l < n; l++) {\n      double* y = Y + l * m;"),
+    "hh_sign_fix_row_only": ("for (int64_t i = 0; i < m; i++) Y[j * m + i] = -Y[j * m + i];", ";"),
+    "prequr_hh_RUS_order": ("else orc_trmm(n, U, n, S, n, R, n);\n  }\n  free(S); free(U); free(Y);\n  return info;\n}\n\n/* E = Y^T Y",
+                            "else orc_trmm(n, S, n, U, n, R, n);\n  }\n  free(S); free(U); free(Y);\n  return info;\n}\n\n/* E = Y^T Y"),
+    "dd_orth_euclid_missing_minus_I": ("dd_t s = {k == l ? -1.0 : 0.0, 0.0};\n      for (int64_t i = 0; i < m; i++) s = dd_add_prod(s, Y[k * ldy + i], Y[l * ldy + i]);",
+                                       "dd_t s = {0.0, 0.0};\n      for (int64_t i = 0; i < m; i++) s = dd_add_prod(s, Y[k * ldy + i], Y[l * ldy + i]);"),
     "dd_orth_tridiag_e_index": ("if (i > 0) s = dd_add_prod(s, e[i - 1], q[i - 1]);", "if (i > 0) s = dd_add_prod(s, e[i], q[i - 1]);"),
 }
 
@@ -60,7 +75,7 @@ def main():
             r = subprocess.run(
                 f'{sys.executable} -c "import oracle; oracle.build(force=True)" && '
                 f"{sys.executable} -m pytest tests/test_oracle_pins.py tests/test_oracle_checkers.py "
-                f"tests/test_oracle_stable.py tests/test_oracle_tridiag.py -q -x -p no:cacheprovider 2>&1 | tail -1",
+                f"tests/test_oracle_stable.py tests/test_oracle_tridiag.py tests/test_oracle_hh.py -q -x -p no:cacheprovider 2>&1 | tail -1",
                 shell=True, capture_output=True, text=True, cwd=ROOT)
             line = r.stdout.strip()
             killed = "failed" in line

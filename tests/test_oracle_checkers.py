@@ -252,3 +252,19 @@ def test_dd_orth_tridiag_exact():
         oracle._load().orc_dd_orth_tridiag(m, n, oracle._p(d), oracle._p(e), oracle._p(to_cm(Qx)), m, oracle._p(Ec))
         b = dd_bound(Ee, S, 2 * 3)
         assert np.all(err(Ec.T, Ee) <= b), (err(Ec.T, Ee) / b).max()
+
+
+def test_dd_orth_euclid_exact():
+    """Y^T Y - I for a Householder Y (E = O(u)) and a perturbed one, against exact arithmetic."""
+    m, n = 8, 4
+    rng = np.random.default_rng(14)
+    Y, _ = oracle.hhqr(to_cm(rng.standard_normal((m, n))), m)
+    Yd = from_cm(Y, m)
+    for Yx in (Yd, Yd + 1e-5 * rng.standard_normal((m, n))):
+        Ee, S = _orth_exact(np.eye(m), Yx)
+        E = oracle.dd_orth_euclid_matrix(to_cm(Yx), m)
+        b = dd_bound(Ee, S, m)
+        assert any(v != 0 for row in Ee for v in row)
+        assert np.all(err(E, Ee) <= b), (err(E, Ee) / b).max()
+    Ee, S = _orth_exact(np.eye(m), Yd)
+    assert np.any(err(Yd.T @ Yd - np.eye(n), Ee) > dd_bound(Ee, S, m)), "input does not discriminate"
