@@ -109,12 +109,33 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
+def cpu_model() -> str:
+    try:
+        return next((l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")), "?")
+    except OSError:
+        return "?"
+
+
+def oracle_threads() -> int:
+    """Host threads the oracle runs on: all cores of this process's affinity mask.  torchrun exports
+    OMP_NUM_THREADS=1 to every rank; the oracle (rank 0 alone) is meant to use the whole host, so
+    the variable is overridden before the oracle's OpenMP runtime loads."""
+    t = len(os.sched_getaffinity(0))
+    os.environ["OMP_NUM_THREADS"] = str(t)
+    try:  # already loaded (second call): set the runtime's count directly
+        import ctypes
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(t)
+    except OSError:
+        pass
+    return t
+
+
 def cpu_oracle_sample(p, target_s: float = 12.0, lead=None):
     """Time the CPU oracle (as it stands) on the leading r x r principal block of the config's A
     and the first r rows of Z, with r sized for ~target_s of work.  Returns the cpu_baseline dict."""
     import oracle
     m, n = p.m, p.n
-    threads = len(os.sched_getaffinity(0))
+    threads = oracle_threads()
 
     def run(r):
         # the leading r x r principal block of A (lead(r) when this process holds only a row shard)
@@ -133,7 +154,7 @@ def cpu_oracle_sample(p, target_s: float = 12.0, lead=None):
         r = r2
         dt, _ = run(r)
     return {"value": flops_paper(r, n) / dt / 1e9, "unit": "GFLOP/s", "cores": threads,
-            "kind": "oracle",
+            "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"oracle normal on the leading {r}x{r} principal block of the config's A and "
                       f"first {r} rows of Z (n={n}); {dt:.1f} s; OMP threads={threads}"}, r, dt
 
@@ -172,7 +193,7 @@ def oracle_protocol(configs):
 def reference_arm(args, cfg, rank):
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+    oracle_threads()
     import oracle
     oracle.build()
     c = gen.CONFIGS[cfg]
@@ -192,7 +213,8 @@ def reference_arm(args, cfg, rank):
     base.update(value=v)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"configs[{cfg}] oqr_{args.variant} m={m} n={n}; "
                                                     f"CPU oracle on leading {r}x{r} block",
@@ -264,13 +286,14 @@ def bench_tridiag(args):
     e2e_value = fl / (e0.elapsed_time(e1) / args.e2e_steps * 1e-3) / 1e9
     cpu = None
     if not args.no_cpu_baseline:   # the oracle on the leading mc rows (a tridiagonal of size mc)
-        threads = len(os.sched_getaffinity(0))
+        threads = oracle_threads()
         mc = m          # the whole problem takes well under a second on the host
         Zc = np.ascontiguousarray(p.Z[:, :mc])
         t = time.perf_counter()
         _, _, sto = oracle.VARIANTS_TRIDIAG[args.variant](d[:mc], e[:mc - 1], Zc, mc)
         dt = time.perf_counter() - t
         cpu = {"value": 2.0 * mc * n * n / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": f"oracle {args.variant}_tridiag on the leading {mc} rows (tridiagonal of size {mc}, "
                          f"n={n}); {dt:.1f} s; OMP threads={threads}"}
     traffic = None
@@ -328,7 +351,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--variant", default="normal", choices=["normal", "normal2", "prequr"])
+    ap.add_argument("--variant", default="normal", choices=["normal", "normal2", "prequr", "prequr_hh"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--oracle-protocol", default=None, metavar="CONFIGS",
                     help="SURVEY s8(d) CPU-oracle timing for the given configs (e.g. 0,1,4,2,3) and exit")
@@ -350,6 +373,22 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` outside torchrun: launch the N ranks ourselves (one process per
+        # GPU, torch.distributed.run on 127.0.0.1); never measure 1 GPU under an N-GPU label
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+        os.execv(sys.executable, cmd)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to report a mislabelled line",
+              file=sys.stderr)
+        sys.exit(2)
     if args.oracle_protocol is not None:
         if rank == 0:
             oracle_protocol([int(c) for c in args.oracle_protocol.split(",")])
@@ -390,8 +429,9 @@ def main():
             return Qo, Ro, st
     else:
         # row-sharded strong scaling: this rank generates and holds only its rows
-        from paper_1401_5171_b200.dist import normal_rows, row_partition
-        assert args.variant == "normal", "the row-sharded path implements oqr_normal"
+        from paper_1401_5171_b200.dist import VARIANTS_ROWS, row_partition
+        assert not args.sym, "the row-sharded path streams the dense row blocks of A"
+        rows_fn = VARIANTS_ROWS[args.variant]
         r0, mr = row_partition(m, world)[rank]
         ldar = mr + (mr & 1)
         A_h = pinned((m, ldar))
@@ -400,7 +440,7 @@ def main():
         Q_h = pinned((n, mr))
 
         def step(A, Z):
-            return normal_rows(A, Z, r0, mr)
+            return rows_fn(A, Z, r0, mr)
     fl_gram = 2.0 * mr * m * n  # per K1 launch on this rank
     if args.sym:  # block-lower triangle incl. the 64 x 64 diagonal panels
         fl_gram = 2.0 * n * sum(min(64, m - i0) * min(m, i0 + 64) for i0 in range(0, m, 64))

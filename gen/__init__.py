@@ -18,8 +18,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboqr_gen.so")
 
-REFLECT, BOTTOM, TOP, SPLIT, AORTH = 0, 1, 2, 3, 5
-UCASES = {"reflect": REFLECT, "bottom": BOTTOM, "top": TOP, "split": SPLIT, "aorth": AORTH}
+REFLECT, BOTTOM, TOP, SPLIT, RANDOM, AORTH = 0, 1, 2, 3, 4, 5
+UCASES = {"reflect": REFLECT, "bottom": BOTTOM, "top": TOP, "split": SPLIT, "random": RANDOM, "aorth": AORTH}
+# the paper's case numbers
+PAPER_CASES = {1: "bottom", 2: "top", 3: "split", 4: "random", 5: "aorth"}
 
 SEED_BASE = 0x14015171
 
@@ -58,6 +60,10 @@ def _load():
         lib.oqr_gen_A_rows.restype = ctypes.c_int
         lib.oqr_gen_A_rows.argtypes = [ctypes.c_int64, ctypes.c_double, ctypes.c_uint64, ctypes.c_int64,
                                        ctypes.c_int64, P, ctypes.c_int64]
+        lib.oqr_gen_problem_haar.restype = ctypes.c_int
+        lib.oqr_gen_problem_haar.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_uint64, ctypes.c_int, P, ctypes.c_int64, P, ctypes.c_int64,
+                                             P, P, P, P, P]
         lib.oqr_gen_normal.restype = ctypes.c_double
         lib.oqr_gen_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
         _lib = lib
@@ -130,6 +136,44 @@ def problem(m: int, n: int, kappa_a: float, kappa_z: float, seed: int, ucase: st
     if rc != 0:
         raise ValueError(f"oqr_gen_problem rejected arguments (m={m}, n={n}, ucase={ucase})")
     return Problem(m, n, kappa_a, kappa_z, seed, ucase, A, Z, Yv, Tv, d, s, Yu, Tu, Yw, Tw, cols)
+
+
+@dataclass
+class HaarProblem:
+    """The paper's s7 construction with dense random orthogonal V, W (and U for case 4)."""
+    m: int
+    n: int
+    kappa_a: float
+    kappa_z: float
+    seed: int
+    ucase: str
+    A: np.ndarray | None          # (m, lda) C-order == column-major m x m
+    Z: np.ndarray                 # (n, ldz)
+    V: np.ndarray                 # dense m x m eigenvectors of A (row-major numpy matrix)
+    d: np.ndarray                 # (m,) eigenvalues, descending
+    s: np.ndarray                 # (n,) singular values of Z, descending (case 5: d_J^{-1/2})
+    W: np.ndarray                 # dense n x n right singular vectors
+    cols: np.ndarray              # (n,) V-columns used as left singular vectors, or -1 (case 4)
+
+
+def problem_haar(m: int, n: int, kappa_a: float, kappa_z: float, seed: int, ucase: str = "random",
+                 with_A: bool = True, lda: int | None = None, ldz: int | None = None) -> HaarProblem:
+    """A = V diag(d) V^T with V = orth(randn(m)); Z = U diag(s) W^T with W =
+    orth(randn(n)) and U the case's columns of V (cases 1, 2, 3, 5) or orth(randn(m, n)) (case 4,
+    ucase="random").  m <= 4096 (dense O(m^3) construction).  Padding rows are NaN."""
+    lib = _load()
+    lda = m if lda is None else lda
+    ldz = m if ldz is None else ldz
+    A = np.full((m, lda), np.nan) if with_A else None
+    Z = np.full((n, ldz), np.nan)
+    V = np.empty((m, m)); d = np.empty(m); s = np.empty(n); W = np.empty((n, n))
+    cols = np.empty(n, dtype=np.int64)
+    rc = lib.oqr_gen_problem_haar(m, n, float(kappa_a), float(kappa_z), seed, UCASES[ucase], _ptr(A), lda,
+                                  _ptr(Z), ldz, _ptr(V), _ptr(d), _ptr(s), _ptr(W), _ptr(cols))
+    if rc != 0:
+        raise ValueError(f"oqr_gen_problem_haar rejected arguments (m={m}, n={n}, ucase={ucase})")
+    # V, W come back column-major: V[k] is column k -> transpose to dense matrices
+    return HaarProblem(m, n, kappa_a, kappa_z, seed, ucase, A, Z, V.T.copy(), d, s, W.T.copy(), cols)
 
 
 def A_rows(m: int, kappa_a: float, seed: int, r0: int, r1: int, lda: int | None = None,

@@ -306,3 +306,99 @@ int oqr_gen_problem(int64_t m, int64_t n, double kappa_a, double kappa_z, uint64
   if (Yu) free(Yu);
   return 0;
 }
+
+/*
+ * The paper's s7 construction with DENSE random orthogonal factors:
+ *   V = orth(randn(m)) (Haar), U = the case's columns of V, or orth(randn(m, n)) for case 4
+ *   (random Z), W = orth(randn(n)) (Haar), A = V diag(d) V^T, Z = U diag(s) W^T.
+ * orth() is classical Gram-Schmidt applied twice ("twice is enough") to seeded Gaussian columns,
+ * each column normalised to a positive diagonal of the implied R: the Q factor of a Gaussian
+ * matrix with positive-diagonal R is Haar distributed.  (Gram-Schmidt is NOT on the library's or
+ * the oracle's path; it is used here only to draw random orthogonal matrices.)
+ * Substreams: 4 = V, 5 = U (case 4), 6 = W.  A is formed for i <= j and mirrored (bitwise
+ * symmetric).  O(m^3): for the s7 sweeps (m = 80) and small parity cases (m <= 4096).
+ * Outputs (each may be NULL): V (m x m col-major), d (m), s (n), W (n x n), cols (n).
+ */
+#define OQR_GEN_RANDOM 4
+
+static void orth_gaussian(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* Q) {
+  for (int64_t j = 0; j < cols; j++)
+    for (int64_t i = 0; i < rows; i++) Q[j * rows + i] = oqr_gen_normal(seed, stream, (uint64_t)(j * rows + i));
+  double* h = (double*)malloc(sizeof(double) * (cols > 0 ? cols : 1));
+  for (int64_t j = 0; j < cols; j++) {
+    double* q = Q + j * rows;
+    for (int pass = 0; pass < 2; pass++) {
+      for (int64_t k = 0; k < j; k++) {
+        const double* qk = Q + k * rows;
+        double s = 0.0;
+        for (int64_t i = 0; i < rows; i++) s += qk[i] * q[i];
+        h[k] = s;
+      }
+      for (int64_t k = 0; k < j; k++) {
+        const double* qk = Q + k * rows;
+        for (int64_t i = 0; i < rows; i++) q[i] -= h[k] * qk[i];
+      }
+    }
+    double nrm = 0.0;
+    for (int64_t i = 0; i < rows; i++) nrm += q[i] * q[i];
+    nrm = sqrt(nrm);
+    for (int64_t i = 0; i < rows; i++) q[i] /= nrm;
+  }
+  free(h);
+}
+
+int oqr_gen_problem_haar(int64_t m, int64_t n, double kappa_a, double kappa_z, uint64_t seed, int ucase,
+                         double* A, int64_t lda, double* Z, int64_t ldz, double* V_out, double* d_out,
+                         double* s_out, double* W_out, int64_t* cols_out) {
+  if (m < 1 || n < 1 || n > m || m > 4096 || kappa_a < 1.0 || kappa_z < 1.0) return -1;
+  if (A && lda < m) return -1;
+  if (Z && ldz < m) return -1;
+  if (ucase != OQR_GEN_RANDOM && ucase != OQR_GEN_TOP && ucase != OQR_GEN_BOTTOM && ucase != OQR_GEN_SPLIT &&
+      ucase != OQR_GEN_AORTH) return -1;
+  double* V = (double*)malloc(sizeof(double) * m * m);
+  double* d = (double*)malloc(sizeof(double) * m);
+  double* s = (double*)malloc(sizeof(double) * n);
+  double* W = (double*)malloc(sizeof(double) * n * n);
+  double* Uc = (double*)malloc(sizeof(double) * m * n);
+  int64_t* J = (int64_t*)malloc(sizeof(int64_t) * n);
+  orth_gaussian(m, m, seed, 4, V);
+  oqr_gen_logspace(m, kappa_a, d);
+  orth_gaussian(n, n, seed, 6, W);
+  if (ucase == OQR_GEN_RANDOM) {
+    orth_gaussian(m, n, seed, 5, Uc);
+    for (int64_t k = 0; k < n; k++) J[k] = -1;
+  } else {
+    select_cols(m, n, ucase, J);
+    for (int64_t k = 0; k < n; k++) memcpy(Uc + k * m, V + J[k] * m, sizeof(double) * m);
+  }
+  if (ucase == OQR_GEN_AORTH) {
+    for (int64_t k = 0; k < n; k++) s[k] = 1.0 / sqrt(d[J[k]]);
+  } else {
+    oqr_gen_logspace(n, kappa_z, s);
+  }
+  if (A) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t j = 0; j < m; j++)
+      for (int64_t i = 0; i <= j; i++) {
+        double v = 0.0;
+        for (int64_t k = 0; k < m; k++) v += V[k * m + i] * d[k] * V[k * m + j];
+        A[j * lda + i] = v;
+        A[i * lda + j] = v;
+      }
+  }
+  if (Z) {
+    for (int64_t l = 0; l < n; l++)
+      for (int64_t i = 0; i < m; i++) {
+        double v = 0.0;
+        for (int64_t k = 0; k < n; k++) v += Uc[k * m + i] * s[k] * W[k * n + l];
+        Z[l * ldz + i] = v;
+      }
+  }
+  if (V_out) memcpy(V_out, V, sizeof(double) * m * m);
+  if (d_out) memcpy(d_out, d, sizeof(double) * m);
+  if (s_out) memcpy(s_out, s, sizeof(double) * n);
+  if (W_out) memcpy(W_out, W, sizeof(double) * n * n);
+  if (cols_out) memcpy(cols_out, J, sizeof(int64_t) * n);
+  free(V); free(d); free(s); free(W); free(Uc); free(J);
+  return 0;
+}

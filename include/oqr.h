@@ -202,6 +202,15 @@ int oqr_prequr_hh_async(int64_t m, int64_t n, const double* A, int64_t lda, cons
                         double* Q, double* R, void* workspace, size_t workspace_bytes, int* d_status,
                         oqr_stream_t stream);
 
+/* The library's device memory pool (current device).  Scratch of the calls is stream-ordered from
+ * it; up to 4 GiB of freed blocks stay cached between calls (no driver allocation per call), larger
+ * transient staging (oqr_normal_host's device copy of A) is returned to the driver at the call's
+ * final synchronisation.  oqr_pool_trim synchronises the device and releases cached blocks down to
+ * keep_bytes (0: everything not in use); status 0 or -100.  oqr_pool_reserved: bytes the pool
+ * currently holds from the driver (or -100). */
+int oqr_pool_trim(size_t keep_bytes);
+int64_t oqr_pool_reserved(void);
+
 /* Human-readable text for a status code (static storage; never NULL). */
 const char* oqr_status_string(int status);
 
@@ -219,7 +228,9 @@ int oqr_gram(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z
 int oqr_gram_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
                      double* G, oqr_stream_t stream);
 
-/* G = Z^T Z, the Euclidean Gram of the PRE-CHOLQR pre-step (reading R2). */
+/* G = Z^T Z, the Euclidean Gram of the PRE-CHOLQR pre-step (reading R2).  Unlike the
+ * factorisations, n > m is allowed (a row block of the row-sharded path may hold fewer rows than
+ * columns): -2 only for n < 1 or n > OQR_NMAX. */
 int oqr_gram_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* G,
                     oqr_stream_t stream);
 
@@ -230,9 +241,15 @@ int oqr_potrf(int64_t n, const double* G, double* R, int* d_info, oqr_stream_t s
 
 /* Q = Z R^{-1} by row-wise substitution, Algorithm 1 line 4:
  * q_ij = (z_ij - sum_{k<j} q_ik r_kj) / r_jj.  R: n x n, ld n, upper.  Q: m x n, ld m.
- * Q may equal Z when ldz == m (in-place). */
+ * Q may equal Z when ldz == m (in-place).  n > m is allowed (rows are independent; a row block of
+ * the row-sharded path may hold fewer rows than columns): -2 only for n < 1 or n > OQR_NMAX. */
 int oqr_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, double* Q,
              oqr_stream_t stream);
+
+/* R = R2 R1 for upper triangular n x n R2, R1 (ld n): the R of repeated CHOLQR and R = U S of
+ * PRE-CHOLQR; R[k, l] = sum_{p=k}^{l} R2[k, p] R1[p, l], strictly lower part zero.
+ * Asynchronous.  Status 0, -1 n, -2 R2, -3 R1, -4 R, -100 CUDA. */
+int oqr_trmm(int64_t n, const double* R2, const double* R1, double* R, oqr_stream_t stream);
 
 /* [Y, S] = Householder QR of Z (Algorithm 2 line 1; the pre-step of oqr_prequr_hh):
  * Y m x n (ld m) with orthonormal columns, S n x n (ld n) upper triangular with positive diagonal,

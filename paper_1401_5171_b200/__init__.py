@@ -30,9 +30,9 @@ EXPORTS = ("oqr_normal", "oqr_normal_host", "oqr_normal2", "oqr_prequr", "oqr_wo
            "oqr_prequr_stable_tridiag", "oqr_normal_sym", "oqr_normal2_sym", "oqr_prequr_sym",
            "oqr_gram_sym", "oqr_upload_sym", "oqr_normal_tridiag", "oqr_normal2_tridiag",
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
-           "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_gram_rows", "oqr_sum_partials",
+           "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_trmm", "oqr_gram_rows", "oqr_sum_partials",
            "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_timing_read_kernel",
-           "oqr_launch_count")
+           "oqr_launch_count", "oqr_pool_trim", "oqr_pool_reserved")
 
 
 class OqrError(RuntimeError):
@@ -89,6 +89,8 @@ def lib() -> ctypes.CDLL:
         L.oqr_potrf.argtypes = [I64, P, P, P, P]
         L.oqr_trsm.restype = I
         L.oqr_trsm.argtypes = [I64, I64, P, I64, P, P, P]
+        L.oqr_trmm.restype = I
+        L.oqr_trmm.argtypes = [I64, P, P, P, P]
         L.oqr_hhqr.restype = I
         L.oqr_hhqr.argtypes = [I64, I64, P, I64, P, P, P]
         L.oqr_gram_rows.restype = I
@@ -104,6 +106,10 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(I64)]
         L.oqr_timing_read_kernel.restype = I
         L.oqr_timing_read_kernel.argtypes = [I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
+        L.oqr_pool_trim.restype = I
+        L.oqr_pool_trim.argtypes = [ctypes.c_size_t]
+        L.oqr_pool_reserved.restype = I64
+        L.oqr_pool_reserved.argtypes = []
         L.oqr_launch_count.restype = I64
         L.oqr_launch_count.argtypes = []
         _lib = L
@@ -438,6 +444,32 @@ def trsm_rows(Z, R, r0: int, mr: int, Q=None, stream=None):
     return Q
 
 
+def gram_euclid_rows(Z, r0: int, mr: int, G=None, stream=None):
+    """G_r = Z_R^T Z_R for the rows R = [r0, r0 + mr) of Z (n, ldz) (asynchronous)."""
+    import torch
+    n = Z.shape[0]
+    if G is None:
+        G = torch.empty((n, n), dtype=torch.float64, device=Z.device)
+    _check(Z, "Z", r0 + mr)
+    st = lib().oqr_gram_euclid(mr, n, ctypes.c_void_p(Z.data_ptr() + 8 * r0), Z.shape[1], _check(G, "G", n),
+                               _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_gram_euclid")
+    return G
+
+
+def trmm(R2, R1, R=None, stream=None):
+    """R = R2 R1 for upper triangular (n, n) tensors (asynchronous step export)."""
+    import torch
+    n = R1.shape[0]
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=R1.device)
+    st = lib().oqr_trmm(n, _check(R2, "R2", n), _check(R1, "R1", n), _check(R, "R", n), _stream(stream))
+    if st:
+        raise OqrError(st, "oqr_trmm")
+    return R
+
+
 def workspace_bytes(m: int, n: int) -> int:
     """Bytes of caller workspace the *_async calls need (upper bound over all variants)."""
     return int(lib().oqr_workspace_bytes(m, n))
@@ -511,6 +543,18 @@ def timing_read() -> tuple[float, int, int]:
     if st:
         raise OqrError(st, "oqr_timing_read")
     return ms.value, k1.value, tot.value
+
+
+def pool_trim(keep_bytes: int = 0) -> None:
+    """Release the library pool's cached device memory down to keep_bytes (synchronises the device)."""
+    st = lib().oqr_pool_trim(int(keep_bytes))
+    if st:
+        raise OqrError(st, "oqr_pool_trim")
+
+
+def pool_reserved() -> int:
+    """Bytes of device memory the library pool currently holds."""
+    return int(lib().oqr_pool_reserved())
 
 
 def launch_count() -> int:

@@ -57,8 +57,12 @@ void timing_end(cudaStream_t s) {
 }
 
 // The library's own stream-ordered memory pool per device (never the device's default pool, whose
-// settings belong to the caller): freed blocks stay cached, so the per-call
-// cudaMallocFromPoolAsync / cudaFreeAsync pair costs no driver allocation after the first call.
+// settings belong to the caller): freed blocks up to OQR_POOL_KEEP bytes stay cached, so the
+// per-call cudaMallocFromPoolAsync / cudaFreeAsync pair of the device-resident calls (tens of MB)
+// costs no driver allocation after the first call, while larger transient staging (the device
+// copy of A in oqr_normal_host: 12.8 GB at m = 40000) goes back to the driver at the call's final
+// stream synchronisation instead of staying reserved.  oqr_pool_trim releases the rest on demand.
+static constexpr uint64_t OQR_POOL_KEEP = 4ull << 30;
 static cudaMemPool_t library_pool() {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
@@ -72,7 +76,7 @@ static cudaMemPool_t library_pool() {
     props.location.id = dev;
     cudaMemPool_t pool;
     if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
-    uint64_t thr = UINT64_MAX;
+    uint64_t thr = OQR_POOL_KEEP;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     pools[dev] = pool;
   }
@@ -165,10 +169,12 @@ static int cuda_status(cudaError_t e) {
 
 static bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+// wide: n > m allowed (row blocks of the row-sharded path: the Euclidean Gram and the row-wise
+// substitution of a block with fewer rows than columns are well defined)
 static int check_args(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
-                      const double* Q, const double* R, bool needA, bool needQR) {
+                      const double* Q, const double* R, bool needA, bool needQR, bool wide = false) {
   if (m < 1) return -1;
-  if (n < 1 || n > m || n > OQR_NMAX) return -2;
+  if (n < 1 || (n > m && !wide) || n > OQR_NMAX) return -2;
   if (needA) {
     if (A == nullptr || !aligned(A, 8)) return -3;
     if (lda < m) return -4;
@@ -712,7 +718,7 @@ int oqr_sum_partials(int64_t n, int64_t count, const double* P, double* G, oqr_s
 }
 
 int oqr_gram_euclid(int64_t m, int64_t n, const double* Z, int64_t ldz, double* G, oqr_stream_t stream) {
-  int st = check_args(m, n, nullptr, m, Z, ldz, nullptr, nullptr, false, false);
+  int st = check_args(m, n, nullptr, m, Z, ldz, nullptr, nullptr, false, false, true);
   if (st) return st;
   if (G == nullptr) return -7;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -730,10 +736,33 @@ int oqr_potrf(int64_t n, const double* G, double* R, int* d_info, oqr_stream_t s
 
 int oqr_trsm(int64_t m, int64_t n, const double* Z, int64_t ldz, const double* R, double* Q,
              oqr_stream_t stream) {
-  int st = check_args(m, n, nullptr, m, Z, ldz, Q, R, false, true);
+  int st = check_args(m, n, nullptr, m, Z, ldz, Q, R, false, true, true);
   if (st) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return cuda_status(launch_trsm(m, (int)n, Z, ldz, R, n, Q, m, nullptr, s));
+}
+
+int oqr_trmm(int64_t n, const double* R2, const double* R1, double* R, oqr_stream_t stream) {
+  if (n < 1 || n > OQR_NMAX) return -1;
+  if (R2 == nullptr || !aligned(R2, 8)) return -2;
+  if (R1 == nullptr || !aligned(R1, 8)) return -3;
+  if (R == nullptr || !aligned(R, 8)) return -4;
+  return cuda_status(launch_trmm((int)n, R2, R1, R, nullptr, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int oqr_pool_trim(size_t keep_bytes) {
+  cudaMemPool_t pool = library_pool();
+  if (pool == nullptr) return -100;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -100;
+  return cuda_status(cudaMemPoolTrimTo(pool, keep_bytes));
+}
+
+int64_t oqr_pool_reserved(void) {
+  cudaMemPool_t pool = library_pool();
+  uint64_t v = 0;
+  if (pool == nullptr || cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v) != cudaSuccess)
+    return -100;
+  return (int64_t)v;
 }
 
 void oqr_timing_enable(int enable) { g_timing = enable != 0; }

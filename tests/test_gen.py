@@ -100,3 +100,41 @@ def test_input_bytes_match_the_recorded_hashes():
         assert f"configs[{k}] m={p.m} n={p.n}  A {sha(p.A)}  Z {sha(p.Z)}" in rec
     d, e, p = gen.tridiag_config("t")
     assert f"tridiag t m={p.m} n={p.n}  d {sha(d)}  e {sha(e)}  Z {sha(p.Z)}" in rec
+
+
+@pytest.mark.parametrize("ucase", ["random", "top", "bottom", "split", "aorth"])
+def test_haar_construction(ucase):
+    """PAPER.md:743-756 with dense random orthogonal V, W (and U, case 4): V orthogonal, A bitwise
+    symmetric with eigenpairs (d, V), Z = U diag(s) W^T with orthonormal U, W."""
+    m, n = 80, 10
+    p = gen.problem_haar(m, n, 1e6, 1e3, 7, ucase)
+    V, W = p.V, p.W
+    assert np.abs(V.T @ V - np.eye(m)).max() < 1e-14
+    assert np.abs(W.T @ W - np.eye(n)).max() < 1e-14
+    A, Z = _dense(p.A, m), _dense(p.Z, m)
+    assert np.array_equal(A, A.T)
+    assert np.abs(A @ V - V * p.d).max() < 1e-14
+    sv = np.linalg.svd(Z, compute_uv=False)
+    assert np.abs(sv - np.sort(p.s)[::-1]).max() <= 1e-14 * p.s.max()
+    if ucase == "random":
+        assert list(p.cols) == [-1] * n
+        # a Haar U is not aligned with any few eigenvectors: every eigen-direction carries weight
+        Uz = np.linalg.svd(Z, full_matrices=False)[0]
+        w = np.linalg.norm(V.T @ Uz, axis=1)
+        assert w.min() > 1e-3 and w.max() < 0.9
+    else:
+        J = p.cols
+        P = V[:, J] @ V[:, J].T
+        assert np.abs(P @ Z - Z).max() < 1e-13 * np.abs(Z).max()
+    if ucase == "aorth":
+        assert np.abs(Z.T @ A @ Z - np.eye(n)).max() < 100 * m * 2.0 ** -53 * p.kappa_a   # u ||Z||^2 ||A||
+
+
+def test_haar_deterministic_and_substreams():
+    a = gen.problem_haar(40, 5, 1e3, 1e2, 3, "random")
+    b = gen.problem_haar(40, 5, 1e3, 1e2, 3, "random", lda=41, ldz=43)
+    assert np.array_equal(a.A, b.A[:, :40]) and np.array_equal(a.Z, b.Z[:, :40])
+    assert np.all(np.isnan(b.A[:, 40:])) and np.all(np.isnan(b.Z[:, 40:]))
+    c = gen.problem_haar(40, 5, 1e3, 1e2, 3, "top")
+    assert np.array_equal(a.A, c.A)                 # V depends on the seed only
+    assert not np.array_equal(a.Z, c.Z)

@@ -44,3 +44,22 @@ def test_threads_on_separate_streams_bitwise():
     for (i, v, rep), (Q, R) in results.items():
         Qr, Rr = ref[(i, v)]
         assert torch.equal(Q, Qr) and torch.equal(R, Rr), (i, v, rep)
+
+
+def test_pool_releases_host_call_staging():
+    """oqr_normal_host stages A in device memory from the library pool; a staging buffer above the
+    pool's 4 GiB release threshold is not kept reserved after the call, and
+    oqr_pool_trim(0) empties the pool."""
+    import numpy as np
+    import paper_1401_5171_b200 as oqr
+    m, n = 24000, 16                       # A = 4.6 GB > 4 GiB
+    A = torch.empty((m, m), dtype=torch.float64)
+    A.fill_(0.0)
+    A.view(-1)[:: m + 1] = 2.0             # 2 I: SPD, trivially factorable
+    Z = torch.from_numpy(np.ascontiguousarray(np.eye(m, n).T))
+    Q, R, st = oqr.normal_host(A, Z)
+    assert st == 0
+    assert torch.allclose(R, 2.0 ** 0.5 * torch.eye(n, dtype=torch.float64))
+    assert oqr.pool_reserved() < m * m * 8
+    oqr.pool_trim(0)
+    assert oqr.pool_reserved() == 0

@@ -27,9 +27,9 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, variant="normal"):
     import torch.distributed as dist
-    from paper_1401_5171_b200.dist import normal_rows, row_partition
+    from paper_1401_5171_b200.dist import VARIANTS_ROWS, row_partition
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -38,7 +38,7 @@ def _worker(rank, world, port, out):
         ldar = mr + (mr & 1)
         Ar = torch.from_numpy(gen.A_rows(M, KA, SEED, r0, r0 + mr, lda=ldar)).cuda()
         p = gen.problem(M, N, KA, KZ, SEED, with_A=False)
-        Q, R, st = normal_rows(Ar, torch.from_numpy(p.Z).cuda(), r0, mr)
+        Q, R, st = VARIANTS_ROWS[variant](Ar, torch.from_numpy(p.Z).cuda(), r0, mr)
         torch.cuda.synchronize()
         np.save(os.path.join(out, f"R{rank}.npy"), R.cpu().numpy())
         np.save(os.path.join(out, f"Q{rank}.npy"), Q.cpu().numpy())
@@ -73,3 +73,25 @@ def test_two_ranks_one_gpu_gloo(tmp_path):
         Gs.append(oqr.gram_rows(torch.from_numpy(gen.A_rows(M, KA, SEED, r0, r0 + mr, lda=ldar)).cuda(), Z, r0, mr))
     R, info = oqr.potrf(oqr.sum_partials(torch.stack(Gs)))
     assert int(info.item()) == 0 and np.array_equal(R.cpu().numpy(), R0)
+
+
+@pytest.mark.parametrize("variant", ["normal2", "prequr", "prequr_hh"])
+def test_two_ranks_one_gpu_gloo_variants(tmp_path, variant):
+    """The two-exchange variants (repeated CHOLQR, Cholesky-QR PRE-CHOLQR) and the Householder
+    PRE-CHOLQR over two real ranks: same R bits on both, Theorem 3 / oracle-relative gates."""
+    import torch.multiprocessing as mp
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), variant), nprocs=world, join=True,
+                       start_method="spawn")
+    assert open(tmp_path / "st0").read() == open(tmp_path / "st1").read() == "0"
+    R0, R1 = np.load(tmp_path / "R0.npy"), np.load(tmp_path / "R1.npy")
+    assert np.array_equal(R0, R1)
+    Q = np.concatenate([np.load(tmp_path / f"Q{r}.npy") for r in range(world)], axis=1)
+    p = gen.problem(M, N, KA, KZ, SEED)
+    Qo, Ro, sto = oracle.VARIANTS[variant](p.A, p.Z, M)
+    assert sto == 0
+    rho, rho_o = oracle.componentwise_ratio(p.Z, Q, R0, M), oracle.componentwise_ratio(p.Z, Qo, Ro, M)
+    assert rho <= 10 * rho_o + 4 * gamma(N + 1)
+    E, Eo = oracle.orth_error(p.A, Q, M), oracle.orth_error(p.A, Qo, M)
+    normQ = np.linalg.norm(oracle.from_cm(Qo, M), 2)
+    assert E <= 10 * Eo + 10 * N * U * float(np.max(p.d)) * normQ ** 2

@@ -91,3 +91,46 @@ def test_normal_rows_over_a_one_rank_nccl_group(oqr):
         assert torch.equal(R1, R2) and torch.equal(Q1, Q2)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_hh"])
+def test_rows_variants_world1_bitwise(oqr, variant):
+    """With one shard every row-sharded variant runs exactly the single-GPU call's kernels: bitwise
+    equal results (repeated CHOLQR and both PRE-CHOLQRs included)."""
+    from paper_1401_5171_b200.dist import VARIANTS_ROWS
+    p = gen.problem(900, 37, 1e3, 1e3, 5)
+    A = torch.from_numpy(p.A).cuda()
+    Z = torch.from_numpy(p.Z).cuda()
+    Q1, R1, s1 = VARIANTS_ROWS[variant](A, Z, 0, 900)
+    Q2, R2, s2 = oqr.VARIANTS[variant](A, Z)
+    assert s1 == s2 == 0
+    assert torch.equal(R1, R2) and torch.equal(Q1, Q2)
+
+
+@pytest.mark.parametrize("mr", [1, 5, 17, 39])
+def test_wide_row_blocks(oqr, mr):
+    """Row blocks with fewer rows than columns (n = 40): the Euclidean Gram of the block and the
+    row-wise substitution (oqr_gram_euclid / oqr_trsm accept n > m), against the oracle."""
+    m, n, r0 = 300, 40, 101
+    p = gen.problem(m, n, 1.0, 1e2, 6, with_A=False)
+    Z = torch.from_numpy(p.Z).cuda()
+    G = oqr.gram_euclid_rows(Z, r0, mr).cpu().numpy().T
+    Zb = oracle.from_cm(p.Z, m)[r0:r0 + mr]
+    Go = oracle.from_cm(oracle.gram_euclid(oracle.to_cm(Zb), mr), n)
+    assert np.all(np.abs(G - Go) <= 2 * gamma(3 * mr) * (np.abs(Zb).T @ np.abs(Zb)))
+    Rs, _ = oracle.potrf(oracle.gram_euclid(p.Z, m))
+    Q = oqr.trsm_rows(Z, torch.from_numpy(Rs).cuda(), r0, mr).cpu().numpy()
+    Qo = oracle.trsm(oracle.to_cm(Zb), Rs, mr)
+    assert oracle.componentwise_ratio(oracle.to_cm(Zb), Q, Rs, mr) <= gamma(n + 1)
+    assert np.linalg.norm(Q - Qo) <= 2 * gamma(n + 1) * np.linalg.norm(np.abs(oracle.from_cm(Qo, mr)) @ np.abs(
+        oracle.from_cm(Rs, n))) / np.linalg.svd(oracle.from_cm(Rs, n), compute_uv=False)[-1]
+
+
+def test_trmm_export(oqr):
+    rng = np.random.default_rng(9)
+    n = 37
+    R2, R1 = np.triu(rng.standard_normal((n, n))), np.triu(rng.standard_normal((n, n)))
+    R = oqr.trmm(torch.from_numpy(oracle.to_cm(R2)).cuda(), torch.from_numpy(oracle.to_cm(R1)).cuda()).cpu().numpy()
+    Ro = oracle.trmm(oracle.to_cm(R2), oracle.to_cm(R1))
+    assert np.array_equal(np.tril(oracle.from_cm(R, n), -1), np.zeros((n, n)))
+    assert np.all(np.abs(R - Ro) <= 2 * gamma(n) * oracle.to_cm(np.abs(R2) @ np.abs(R1)))

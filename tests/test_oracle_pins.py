@@ -389,3 +389,43 @@ def test_dd_orth_cols_equals_full_checker_bitwise():
     cols = [0, 3, 7, 11]
     Es = oracle.dd_orth_cols(p.A, Q, p.m, cols)
     assert np.array_equal(Es, E[np.ix_(cols, cols)])
+
+
+# ------------------------------------------------- P2 / P5 on the paper's dense Haar V ---------
+@pytest.mark.parametrize("ucase", ["random", "top", "bottom", "split"])
+def test_p2_theorem1_haar(ucase):
+    """sigma_i(R) = sigma_i(A^{1/2} Z) (Theorem 1) on the s7 construction with a
+    dense random V: A^{1/2} = V diag(sqrt d) V^T exactly from the generator's factors."""
+    m, n = 80, 10
+    p = gen.problem_haar(m, n, 1e6, 1e3, 11, ucase)
+    _, R, info = oracle.normal(p.A, p.Z, m)
+    assert info == 0
+    Zd, Ad = dense(p.Z, m), dense(p.A, m)
+    X = p.V @ (np.sqrt(p.d)[:, None] * (p.V.T @ Zd))
+    sx = svals(X)
+    sr = svals(dense(R, n))
+    # the Gram error is ~ sqrt(m) u ||M||, M = |Z|^T|A||Z| (eq.mult1-2); case 1 cancels in A Z, so
+    # relative to ||G|| = sigma_1(X)^2 it carries the factor ||M|| / sigma_1(X)^2
+    canc = np.linalg.norm(np.abs(Zd).T @ np.abs(Ad) @ np.abs(Zd), 2) / sx[0] ** 2
+    assert np.all(np.abs(sr - sx) / sx <= 10 * np.sqrt(m) * U * canc * (sx[0] / sx) ** 2)
+
+
+def test_p5_haar_closed_forms():
+    """Case 2 constant ||A|| ||Q||^2 = 10^{54/79} at kappa(A) = 1e6 (golden), case 1/3
+    constant kappa(A), case 5 R = I, on the dense-V construction."""
+    g = GOLDEN["case2_orth_constant"]
+    m, n, ka = g["m"], g["n"], g["kappa_a"]
+    p = gen.problem_haar(m, n, ka, 1e2, 12, "top")
+    Q, _, info = oracle.normal(p.A, p.Z, m)
+    assert info == 0
+    assert abs(np.log10(np.linalg.norm(dense(Q, m), 2) ** 2 * p.d[0]) - g["normA_normQ2_log10"]) < 1e-9
+    for ucase in ("bottom", "split"):
+        p = gen.problem_haar(m, n, ka, 1e2, 13, ucase)
+        Q, _, info = oracle.normal(p.A, p.Z, m)
+        assert info == 0
+        # computed Q carries CHOLQR's forward error ~ u kappa(A^{1/2} Z)^2 ||M|| / ||G|| ~ 1e-6 here
+        assert abs(np.linalg.norm(dense(Q, m), 2) ** 2 * p.d[0] / ka - 1.0) < 1e-4
+    p = gen.problem_haar(m, n, 1e8, 1.0, 14, "aorth")
+    Q, R, info = oracle.normal(p.A, p.Z, m)
+    assert info == 0
+    assert np.abs(dense(R, n) - np.eye(n)).max() <= 10 * m * U * 1e8

@@ -41,7 +41,7 @@ def main():
         mn, md = t_events(lambda: oqr.hhqr(Z, m=m))
         fl = 4.0 * m * n * n - 4.0 * n ** 3 / 3   # geqrf 2mn^2 - 2n^3/3 + orgqr 2mn^2 - 2n^3/3
         print(f"hhqr m={m} n={n}: min {mn:.3f} ms, median {md:.3f} ms (K6 event {k6:.3f} ms), "
-              f"{fl / mn / 1e9:.1f} GFLOP/s", flush=True)
+              f"{fl / (mn * 1e-3) / 1e9:.1f} GFLOP/s", flush=True)
 
 
 if __name__ == "__main__":
