@@ -533,14 +533,22 @@ def main():
                 p, lead=lambda r: gen.config_A_rows(args.config, 0, r)[:r, :r])
         peaks = measured_peaks()
         line = {
-            "metric": METRIC,
+            # --sym: the symmetric schedule does about half the dense flops; its value is the dense
+            # problem's flops over its time (DENSE-EQUIVALENT rate, can exceed the FP64 peak), so it
+            # is not reported under BASELINE's metric string
+            "metric": METRIC if not args.sym else
+            "oblique-QR dense-equivalent GFLOP/s, symmetric-half A (FP64, 1 B200; 2m^2n+2mn^2 over the time "
+            "of the block-lower-triangle algorithm)",
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"configs[{args.config}] oqr_{args.variant}{'_sym' if args.sym else ''}: m={m}, n={n}, "
                                    f"kappa_A={c['kappa_a']:g}, kappa_Z={c['kappa_z']:g}",
                        "m": m, "n": n, "variant": args.variant,
-                       "flops_per_step": fl, "flop_normalisation": "2m^2n+2mn^2 (PAPER.md:959-961)",
+                       "flops_per_step": fl,
+                       "flop_normalisation": ("dense-equivalent: 2m^2n+2mn^2 (PAPER.md:959-961) although the "
+                                              "symmetric schedule performs ~m^2n+2mn^2") if args.sym else
+                       "2m^2n+2mn^2 (PAPER.md:959-961)",
                        "l2": "inputs (A = %.1f GB) larger than L2; no flush" % (8 * m * m / 1e9),
                        "parallelism": (f"row-sharded x{world}: one n x n all-gather per step (NCCL), "
                                        "fixed rank-order sum") if (world > 1 or args.sharded) else "single GPU"},

@@ -211,6 +211,13 @@ int oqr_prequr_hh_async(int64_t m, int64_t n, const double* A, int64_t lda, cons
 int oqr_pool_trim(size_t keep_bytes);
 int64_t oqr_pool_reserved(void);
 
+/* Which path the fused Gram kernel takes for an A (m x m, lda): 1 = FAST (16-byte aligned A, even
+ * lda: tensor-TMA tiles), 0 = SLOW (8-byte aligned A or odd lda: plain loads for every tile, same
+ * results, several times slower); -1 m < 1, -3 A null or not 8-byte aligned, -4 lda < m.  The
+ * factorisations accept both paths (the argument checks reject only what neither path can read);
+ * callers that need the fast path check it here. */
+int oqr_gram_fast_path(int64_t m, const double* A, int64_t lda);
+
 /* Human-readable text for a status code (static storage; never NULL). */
 const char* oqr_status_string(int status);
 

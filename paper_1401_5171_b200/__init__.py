@@ -32,7 +32,7 @@ EXPORTS = ("oqr_normal", "oqr_normal_host", "oqr_normal2", "oqr_prequr", "oqr_wo
            "oqr_prequr_tridiag", "oqr_gram_tridiag", "oqr_status_string", "oqr_gram",
            "oqr_gram_euclid", "oqr_potrf", "oqr_trsm", "oqr_trmm", "oqr_gram_rows", "oqr_sum_partials",
            "oqr_timing_enable", "oqr_timing_reset", "oqr_timing_read", "oqr_timing_read_kernel",
-           "oqr_launch_count", "oqr_pool_trim", "oqr_pool_reserved")
+           "oqr_launch_count", "oqr_pool_trim", "oqr_pool_reserved", "oqr_gram_fast_path")
 
 
 class OqrError(RuntimeError):
@@ -106,6 +106,8 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(I64)]
         L.oqr_timing_read_kernel.restype = I
         L.oqr_timing_read_kernel.argtypes = [I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
+        L.oqr_gram_fast_path.restype = I
+        L.oqr_gram_fast_path.argtypes = [I64, P, I64]
         L.oqr_pool_trim.restype = I
         L.oqr_pool_trim.argtypes = [ctypes.c_size_t]
         L.oqr_pool_reserved.restype = I64
@@ -543,6 +545,16 @@ def timing_read() -> tuple[float, int, int]:
     if st:
         raise OqrError(st, "oqr_timing_read")
     return ms.value, k1.value, tot.value
+
+
+def gram_fast_path(A) -> bool:
+    """True when the fused Gram kernel reads this A (tensor (m, lda)) through tensor TMA (16-byte
+    aligned, even lda); False for the plain-load slow path."""
+    m = A.shape[0]
+    st = lib().oqr_gram_fast_path(m, _check(A, "A", m), A.shape[1])
+    if st < 0:
+        raise OqrError(st, "oqr_gram_fast_path")
+    return st == 1
 
 
 def pool_trim(keep_bytes: int = 0) -> None:

@@ -204,6 +204,12 @@ static int gram_into(const AOp& op, int64_t m, int n, const double* Z, int64_t l
                      cudaStream_t s) {
   int g = 0;
   if (op.tridiag) {
+    bool done = false;
+    OQR_TRY(launch_gram_tridiag(m, n, op.d, op.e, Z, ldz, ws.P, &g, s, &done));
+    if (done) {  // stencil fused into the Gram, Z read once (K4t)
+      OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s, false, true));
+      return 0;
+    }
     OQR_TRY(launch_pack_zw_tridiag(m, n, op.d, op.e, Z, ldz, ws.Zp, ws.Zc, s));
     // G = Z^T (T Z) is symmetric: upper tiles only, mirrored by the reduction
     OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zc, ws.P, &g, s));
@@ -748,6 +754,13 @@ int oqr_trmm(int64_t n, const double* R2, const double* R1, double* R, oqr_strea
   if (R1 == nullptr || !aligned(R1, 8)) return -3;
   if (R == nullptr || !aligned(R, 8)) return -4;
   return cuda_status(launch_trmm((int)n, R2, R1, R, nullptr, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int oqr_gram_fast_path(int64_t m, const double* A, int64_t lda) {
+  if (m < 1) return -1;
+  if (A == nullptr || !aligned(A, 8)) return -3;
+  if (lda < m) return -4;
+  return (aligned(A, 16) && (lda & 1) == 0) ? 1 : 0;
 }
 
 int oqr_pool_trim(size_t keep_bytes) {

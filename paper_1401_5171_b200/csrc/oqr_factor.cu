@@ -82,11 +82,12 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
         brk = b0 + c + 1;
         break;
       }
-      // one reciprocal square root (<= 1 ulp) on the pivot chain instead of sqrt and then 1/r:
-      // r = d * (1/sqrt(d)) is within ~1.5 ulp of sqrt(d) -- inside the gates' gamma_{n+1}
-      // (PAPER.md:195-196), and 8-16% off K2's time (tools/time_potrf.py)
-      const double inv = rsqrt(d);
-      const double r = d * inv;
+      // r_cc = sqrt(d), correctly rounded (IEEE sqrt, SURVEY s8(a) S2 -- the same r as the
+      // oracle's), and the row scaled by its correctly rounded reciprocal (LAPACK dpotf2's
+      // DSCAL by ONE/AJJ).  (A single rsqrt, r = d * rsqrt(d) within ~1.5 ulp, saved ~8 us at
+      // n = 200; not kept, so the pivot itself is the paper's chol.)
+      const double r = sqrt(d);
+      const double inv = 1.0 / r;
       // row c: (c, c) = r, (c, b > c) *= inv
       if (c < 4) {
         if (ra == c) v0 = (cb == c) ? r : (cb > c ? v0 * inv : v0);
@@ -287,7 +288,11 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
           int jt = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)t)) * 0.5f);
           while (jt * (jt - 1) / 2 > t) --jt;
           while ((jt + 1) * jt / 2 <= t) ++jt;
+#ifdef OQR_EXP_TRSM_LDS128
+          const int kt = t - jt * (jt - 1) / 2, ln = (e >> 1) & 31, h = e & 1;
+#else
           const int kt = t - jt * (jt - 1) / 2, ln = e & 31, h = (e >> 5) & 1;
+#endif
           const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
           if (col < n) v[u] = R[(int64_t)col * ldr + k];
         }
@@ -337,7 +342,10 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
     for (int jt = 0; jt < NT; ++jt) S[jt][0] = S[jt][1] = 0.0;
     // Z of tiles jt+1, jt+2 is loaded before tile jt's Q stores: different columns, so this is
     // safe even in place (Q == Z); the compiler must assume Q aliases Z and would not reorder them.
-    constexpr int PD = 2;  // Z prefetch distance in tiles
+#ifndef OQR_EXP_TRSM_PD
+#define OQR_EXP_TRSM_PD 2
+#endif
+    constexpr int PD = OQR_EXP_TRSM_PD;  // Z prefetch distance in tiles
     double zq[PD][2];
 #pragma unroll
     for (int d = 0; d < PD; ++d)
@@ -383,6 +391,15 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
       // tile, the next one first
       const double a0 = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
       const double a1 = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
+#ifdef OQR_EXP_TRSM_LDS128  // experiment build: both halves' B values in one LDS.128 (h-interleaved Rt)
+#pragma unroll
+      for (int j2 = jt + 1; j2 < NT; ++j2) {
+        double b0, b1;
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(b0), "=d"(b1) : "r"(Rt + 16u * ((j2 * (j2 - 1) / 2 + jt) * 32 + lane)));
+        dmma_f(S[j2], a0, b0);
+        dmma_f(S[j2], a1, b1);
+      }
+#else
       // all first-half k-steps, then all second-half ones: consecutive DMMAs are independent
 #pragma unroll
       for (int j2 = jt + 1; j2 < NT; ++j2)
@@ -390,12 +407,233 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
       for (int j2 = jt + 1; j2 < NT; ++j2)
         dmma_f(S[j2], a1, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + jt) * 64 + 32 + lane)));
+#endif
       // this lane's two C entries -> Q
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = jt * 8 + 2 * q4 + e;
         const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
         if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+      }
+    }
+  }
+}
+
+// ---- K3, warp-pair form (experiment build OQR_EXP_TRSM_PAIR; measured slower) ----------------
+// The same right-looking substitution (the same pieces of the same sums) with the per-tile
+// accumulators of one 8-row block split over a PAIR of warps:
+// warp v of the pair owns the tiles jt with jt % 2 == v (half the registers: twice the warps per
+// SM to hide the diagonal solves' latency).  Tile t's owner solves it, publishes its DMMA
+// A-fragments (2 doubles per lane) in a shared-memory slot and arrives on the pair's mbarrier for
+// t's parity; the partner waits, applies q_t to ITS next tile t+1 at once with DFMA (the only work
+// on the critical path, kept off the tensor pipe whose queue holds the other warps' bulk DMMAs),
+// solves t+1 and publishes it, and only then applies q_t to its later tiles (deferred, DMMA)
+// together with q_{t+1} -- so each warp's bulk DMMA updates overlap the partner's solve.
+// Slots are reused every second tile of a parity: the owner of t+2 waits for q_{t+1}, which its
+// partner publishes only after reading slot t.
+constexpr int TP_GROUPS = 8;  // warp pairs per CTA (16 warps)
+#ifndef OQR_EXP_TP_PD
+#define OQR_EXP_TP_PD 4
+#endif
+constexpr int TP_PD = OQR_EXP_TP_PD;  // Z prefetch distance in own tiles
+
+__device__ __forceinline__ uint32_t tp_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tp_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tp_smem(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tp_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tp_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void tp_mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(tp_smem(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+template <int NT>
+constexpr size_t trsm_pair_smem_bytes() {
+  return trsm_smem_doubles<NT>(true) * sizeof(double) + (size_t)TP_GROUPS * 2 * 64 * sizeof(double) +
+         (size_t)TP_GROUPS * 2 * sizeof(uint64_t);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(TP_GROUPS * 64, 1)
+trsm_pair_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q (in place)
+                 const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info) {
+  if (info != nullptr && *info != 0) return;
+  constexpr int H = (NT + 1) / 2;  // tiles per warp (upper bound)
+  extern __shared__ __align__(16) double rsm[];
+  double* const Rt_base = rsm;
+  double* const Ri_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
+  double* const Rd_base = Ri_base + (size_t)NT * 8;
+  double* const slots = Rd_base + (size_t)NT * 64;                       // [TP_GROUPS][2][2][32]
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(slots + TP_GROUPS * 2 * 64);  // [TP_GROUPS][2]
+  {
+    constexpr int TOT = NT * (NT - 1) / 2 * 64;
+    for (int e0 = threadIdx.x; e0 < TOT; e0 += 8 * TP_GROUPS * 64) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * TP_GROUPS * 64;
+        v[u] = 0.0;
+        if (e < TOT) {
+          const int t = e >> 6;
+          int jt = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)t)) * 0.5f);
+          while (jt * (jt - 1) / 2 > t) --jt;
+          while ((jt + 1) * jt / 2 <= t) ++jt;
+          const int kt = t - jt * (jt - 1) / 2, ln = e & 31, h = (e >> 5) & 1;
+          const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
+          if (col < n) v[u] = R[(int64_t)col * ldr + k];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * TP_GROUPS * 64;
+        if (e < TOT) Rt_base[e] = v[u];
+      }
+    }
+    for (int e = threadIdx.x; e < NT * 64; e += blockDim.x) {
+      const int jt = e >> 6, c = (e >> 3) & 7, c2 = e & 7;
+      const int r = jt * 8 + c, col = jt * 8 + c2;
+      double v = 0.0;
+      if (c <= c2) v = (col < n) ? R[(int64_t)col * ldr + r] : (c == c2 ? 1.0 : 0.0);
+      Rd_base[e] = v;
+    }
+    for (int e = threadIdx.x; e < NT * 8; e += blockDim.x)
+      Ri_base[e] = (e < n) ? 1.0 / R[(int64_t)e * ldr + e] : 1.0;
+    if (threadIdx.x < TP_GROUPS * 2) tp_mbar_init(&bars[threadIdx.x], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp >> 1, v = warp & 1;
+  const int q4 = lane & 3, gbase = lane & ~3;
+  double* const myslot = slots + grp * 2 * 64;
+  uint64_t* const mybars = bars + grp * 2;
+  uint32_t wph = 0;  // phase of the partner's barriers this warp waits on (one completion per wait)
+#pragma unroll 1
+  for (int64_t r0 = ((int64_t)blockIdx.x * TP_GROUPS + grp) * 8; r0 < m; r0 += (int64_t)gridDim.x * TP_GROUPS * 8) {
+    const int64_t row = r0 + (lane >> 2);
+    const bool row_ok = row < m;
+    uint32_t Rt = (uint32_t)__cvta_generic_to_shared(Rt_base);
+    uint32_t Rd = (uint32_t)__cvta_generic_to_shared(Rd_base);
+    uint32_t Ri = (uint32_t)__cvta_generic_to_shared(Ri_base);
+    int64_t ldz_l = ldz, ldq_l = ldq;
+    int n_l = n;
+    asm volatile("" : "+r"(Rt), "+r"(Rd), "+r"(Ri), "+l"(ldz_l), "+l"(ldq_l), "+r"(n_l));
+    double S[H][2];
+#pragma unroll
+    for (int h = 0; h < H; ++h) S[h][0] = S[h][1] = 0.0;
+    // Z of this warp's own tiles, prefetched TP_PD own tiles ahead (a global load's latency spans
+    // several tile solves: ncu showed the subtraction z - S waiting on it with one tile ahead)
+    double zq[TP_PD][2];
+#pragma unroll
+    for (int d = 0; d < TP_PD; ++d)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tt = v + 2 * d, col = tt * 8 + 2 * q4 + e;
+        zq[d][e] = (row_ok && tt < NT && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+      }
+    double d0 = 0.0, d1 = 0.0;  // deferred fragments of the partner's last tile
+    int dt = -1;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      if ((t & 1) == v) {
+        // ---- own tile t: S[t/2] holds every q_k R[k, t], k < t
+        const int h = t >> 1;
+        const double zc0 = zq[h % TP_PD][0], zc1 = zq[h % TP_PD][1];
+        if (t + 2 * TP_PD < NT) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = (t + 2 * TP_PD) * 8 + 2 * q4 + e;
+            zq[h % TP_PD][e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+          }
+        }
+        double t0 = zc0 - S[t >> 1][0];
+        double t1 = zc1 - S[t >> 1][1];
+        double tt[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          tt[2 * q] = __shfl_sync(0xffffffffu, t0, gbase | q);
+          tt[2 * q + 1] = __shfl_sync(0xffffffffu, t1, gbase | q);
+        }
+        double qv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int dc = t * 8 + c;
+          qv[c] = tt[c] * lds_f64(Ri + 8u * dc);
+#pragma unroll
+          for (int c2 = c + 1; c2 < 8; ++c2) tt[c2] = fma(-qv[c], lds_f64(Rd + 8u * ((t * 8 + c) * 8 + c2)), tt[c2]);
+        }
+        const double a0 = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
+        const double a1 = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
+        if (t + 1 < NT) {  // publish the solved 8 x 8 tile, row-major, for the partner
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+            myslot[(t & 1) * 64 + (lane >> 2) * 8 + 2 * q4 + e] = qe;
+          }
+          __syncwarp();
+          if (lane == 0) tp_mbar_arrive(&mybars[t & 1]);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = t * 8 + 2 * q4 + e;
+          const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+          if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+        }
+        // ---- bulk: the deferred q_{t-1} (partner's) and then q_t on this warp's tiles > t, in k
+        // order (first halves, then second halves, per k: the same order as the one-warp kernel)
+        if (dt >= 0) {
+#pragma unroll
+          for (int j2 = t + 2; j2 < NT; j2 += 2)
+            dmma_f(S[j2 >> 1], d0, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + (t - 1)) * 64 + lane)));
+#pragma unroll
+          for (int j2 = t + 2; j2 < NT; j2 += 2)
+            dmma_f(S[j2 >> 1], d1, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + (t - 1)) * 64 + 32 + lane)));
+        }
+#pragma unroll
+        for (int j2 = t + 2; j2 < NT; j2 += 2)
+          dmma_f(S[j2 >> 1], a0, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + t) * 64 + lane)));
+#pragma unroll
+        for (int j2 = t + 2; j2 < NT; j2 += 2)
+          dmma_f(S[j2 >> 1], a1, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + t) * 64 + 32 + lane)));
+        dt = -1;
+      } else {
+        // ---- partner's tile t: wait for q_t (published only when a tile follows), apply it to
+        // this warp's next tile t+1 at once, the rest deferred
+        if (t + 1 < NT) {
+          tp_mbar_wait(&mybars[t & 1], wph);  // the partner's parity: one completion per its tile
+          wph ^= 1u;
+          double qr[8];                        // row lane/4 of q_t
+#pragma unroll
+          for (int k = 0; k < 8; ++k) qr[k] = myslot[(t & 1) * 64 + (lane >> 2) * 8 + k];
+          d0 = (q4 == 0) ? qr[0] : (q4 == 1) ? qr[1] : (q4 == 2) ? qr[2] : qr[3];
+          d1 = (q4 == 0) ? qr[4] : (q4 == 1) ? qr[5] : (q4 == 2) ? qr[6] : qr[7];
+          // the critical update S[t+1] += q_t R[t, t+1] on the FP64 FMA pipe, not behind the
+          // queued bulk DMMAs of the tensor pipe: this lane's C entries (row lane/4, columns
+          // 2 q4 + e) read R[t*8 + k, (t+1)*8 + 2 q4 + e] from the B-fragment tile (t+1, t)
+          const uint32_t rtile = Rt + 8u * (((t + 1) * t / 2 + t) * 64);
+#ifdef OQR_EXP_TP_DMMA_CRIT  // experiment build: the critical update on the tensor pipe too
+          dmma_f(S[(t + 1) >> 1], d0, lds_f64(rtile + 8u * lane));
+          dmma_f(S[(t + 1) >> 1], d1, lds_f64(rtile + 8u * (32 + lane)));
+#else
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              S[(t + 1) >> 1][e] = fma(qr[k], lds_f64(rtile + 8u * ((k >> 2) * 32 + (k & 3) + 4 * (2 * q4 + e))),
+                                       S[(t + 1) >> 1][e]);
+#endif
+          dt = t;
+        }
       }
     }
   }
@@ -411,6 +649,21 @@ static int trsm_num_sms() {
 template <int NT>
 static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
                            double* Q, int64_t ldq, const int* info, cudaStream_t s) {
+#ifdef OQR_EXP_TRSM_PAIR  // experiment build only: the warp-pair kernel (measured slower)
+  if constexpr (NT >= 2 && trsm_pair_smem_bytes<NT>() <= (size_t)SMEM_MAX) {
+    constexpr size_t bytes = trsm_pair_smem_bytes<NT>();
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(trsm_pair_kernel<NT>), (int)bytes);
+    if (e != cudaSuccess) return e;
+    int64_t g = cdiv(m, TP_GROUPS * 8);
+    const int sms = trsm_num_sms();
+    if (g > sms) g = sms;
+    timing_begin(s, OQR_TIMING_K3);
+    trsm_pair_kernel<NT><<<(unsigned)g, TP_GROUPS * 64, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
+    e = cudaGetLastError();
+    timing_end(s);
+    return e;
+  }
+#endif
   constexpr bool smem_rd = trsm_smem_doubles<NT>(true) * sizeof(double) <= (size_t)SMEM_MAX;
   constexpr size_t bytes = trsm_smem_doubles<NT>(smem_rd) * sizeof(double);
   static_assert(bytes <= (size_t)SMEM_MAX, "R fragments must fit in shared memory");

@@ -352,7 +352,7 @@ __host__ __device__ __forceinline__ int unit_nk(int I, int KB) {
 // (~panel_w units of time), so the split equalises W(u) = u + panel_w * (panels started before
 // u) instead of u alone -- the symmetric schedule has panels of 4 .. KB units.  The contraction
 // is ~NT times costlier than one unit relative to the unit's NT-proportional work, so
-// panel_w = PANEL_W_PER_NT * NT (calibrated on B200: tools/time_k1.py, OQR_PANEL_W overrides).
+// panel_w = PANEL_W_PER_NT * NT (calibrated on B200 with tools/time_k1.py and -DOQR_EXP_PANEL_W builds).
 constexpr double PANEL_W_PER_NT = 2.0;
 
 // SYM: panel I has R (I + 1) units (R = BM / KS), so the units before panel I number R I (I+1)/2.
@@ -959,15 +959,216 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
   const int alay = (mr % 8) != 0 ? ALAY_COL : (NT == 1 ? ALAY_R8 : ALAY_R4);
   const bool tma_ok = make_tmap_a(&tmap, A, mr, m, lda, KS, alay);
   timing_begin(s, OQR_TIMING_K1);
-  static const char* env_w = getenv("OQR_PANEL_W");
-  // panel weight in units: a unit carries KS/16 times the work of a 16-wide unit
-  const double panel_w = env_w ? atof(env_w) : PANEL_W_PER_NT * NT * (16.0 / KS);
+  // panel weight in units: a unit carries KS/16 times the work of a 16-wide unit.  (Experiment
+  // builds may override the weight at compile time, -DOQR_EXP_PANEL_W=<w>: it changes the unit
+  // split and so the summation order; the product build has no run-time knob, so results are
+  // bitwise reproducible for a given (m, n, SM count) as include/oqr.h states.)
+#ifdef OQR_EXP_PANEL_W
+  const double panel_w = OQR_EXP_PANEL_W;
+#else
+  const double panel_w = PANEL_W_PER_NT * NT * (16.0 / KS);
+#endif
   gram_fused_kernel<NT, SYM><<<(unsigned)g, NCW * 32, bytes, s>>>(tmap, m, mr, A, lda, Zp, Zc, Zh, P, (int)KB,
                                                                   (int)U, stages, tma_ok, alay, panel_w, accum);
   note_launch();
   cudaError_t e = cudaGetLastError();
   timing_end(s);
   return e;
+}
+
+// ------------------------------------------------------------------ K4t -------------------
+// Tridiagonal Gram with the stencil fused in (NEXT-N3): the upper tiles of G = Z^T (T Z) for
+// T = tridiag(e, d, e), reading Z ONCE, straight from the caller's column-major array -- no packed
+// copies of Z and T Z through HBM.  Per 16-row block b, one 2-D tensor-TMA request lands the
+// 20 x NP box of Z starting at row 16 b - 2 (two halo rows above, two below -- the box start must be
+// 16-byte aligned, so an even row (tools/tma_halo_probe.cu: an odd start row is an illegal
+// instruction); rows outside 0..m-1 and columns >= n zero-filled) as [column][20 rows] in a ring
+// stage -- the 20-double column stride makes every DMMA fragment load bank-conflict-free.  All threads then form the block's
+// W = T Z in DMMA B-fragment order in a double-buffered shared buffer (the same arithmetic as the
+// packing kernel: w = e_{i-1} z_{i-1}; w = fma(d_i, z_i, w); w = fma(e_i, z_{i+1}, w)) -- each
+// block's W formed while the previous block's DMMAs drain, one CTA barrier per block -- and the
+// warps run the upper-tile DMMA schedule of gram_packed_pairs_kernel (same tile assignment, same
+// k order: bitwise the same slots) with the A fragments read from the Z box.
+constexpr int TRB = 20;  // rows per Z box: 2 halo rows above, the block's 16, 2 halo rows below
+constexpr int TRH = 2;   // halo rows above (the box starts at the even row 16 b - 2)
+#ifndef OQR_EXP_TRI_PARTS_FROM
+#define OQR_EXP_TRI_PARTS_FROM 22
+#endif
+// CTA parts per K-slice (two parts of half the warps each above this NT: registers)
+__host__ __device__ constexpr int tri_parts(int NT) { return NT >= OQR_EXP_TRI_PARTS_FROM ? 2 : 1; }
+__host__ __device__ constexpr int tri_warps(int NT) { return (NT + tri_parts(NT) - 1) / tri_parts(NT); }
+
+template <int NT>
+__global__ void __launch_bounds__(32 * tri_warps(NT), 1)
+gram_tridiag_kernel(const __grid_constant__ CUtensorMap zmap, const double* __restrict__ d,
+                    const double* __restrict__ e, int64_t m, int nblk, double* __restrict__ P, int stages) {
+  constexpr int NP = NT * 8;
+  constexpr int T = pairs_tiles(NT);
+  constexpr int NW = tri_warps(NT);
+  constexpr int TILE = TRB * NP;           // doubles per Z box
+  constexpr int WB = NT * 4 * FRAG;        // doubles per W block (fragment order)
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  double* wbuf = reinterpret_cast<double*>(smem + 256);   // [2][WB]
+  double* ring = wbuf + 2 * WB;                           // [stages][TILE]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slice = blockIdx.x, nslices = gridDim.x;
+  const int b0 = (int)((int64_t)nblk * slice / nslices), b1 = (int)((int64_t)nblk * (slice + 1) / nslices);
+  const uint64_t pol = policy_evict_first();  // Z is streamed once
+  constexpr uint32_t TILE_BYTES = TILE * 8;
+  // this slice's diagonal and the couplings of its rows (and the row above), staged once so that
+  // forming W is shared-memory only: ds[i] = d_{16 b0 + i}, es[i] = e_{16 b0 + i - 1} (0 outside)
+  double* ds = ring + stages * TILE;
+  double* es = ds + (b1 - b0) * BK;
+  {
+    const int64_t rs = (int64_t)b0 * BK;
+    const int nr = (b1 - b0) * BK;
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
+      const int64_t row = rs + i;
+      if (i < nr) ds[i] = row < m ? __ldg(d + row) : 0.0;
+      es[i] = (row >= 1 && row - 1 < m - 1) ? __ldg(e + row - 1) : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+    for (int s = 0; s < stages && b0 + s < b1; ++s) {
+      mbar_arrive_expect_tx(&full[s], TILE_BYTES);
+      tma_g2s_2d(ring + s * TILE, &zmap, (b0 + s) * BK - TRH, 0, &full[s], pol);
+    }
+  }
+  __syncthreads();
+  const int g = blockIdx.y * NW + warp;
+  int ka = 0, la0 = 0, len1 = 0, kb = 0, lb0 = 0, len = 0;
+  if (g < NT) {
+    const int i = g >> 1;
+    if ((NT & 1) && g == NT - 1) {
+      ka = i; la0 = i; len1 = len = NT - i;
+    } else if ((g & 1) == 0) {
+      ka = i; la0 = i; len1 = len = T;
+    } else {
+      ka = i; la0 = i + T; len1 = NT - i - T;
+      kb = NT - 1 - i; lb0 = NT - 1 - i; len = len1 + i + 1;
+    }
+  }
+  double acc[T][2];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
+  // block b lives in stage (b - b0) % stages, phase ((b - b0) / stages) & 1
+  auto stage_of = [&](int b) { return (b - b0) % stages; };
+  auto phase_of = [&](int b) { return (uint32_t)(((b - b0) / stages) & 1); };
+  // W(b) = T Z on block b's rows, in B-fragment order, by all threads (Zt[c * TRB + TRH + r] =
+  // Z[16 b + r, c], r = -2 .. 17)
+  auto form_w = [&](int b) {
+    const double* Zt = ring + stage_of(b) * TILE;
+    double* W = wbuf + (b & 1) * WB;
+    const int64_t r0 = (int64_t)b * BK;
+    for (int f = threadIdx.x; f < WB; f += blockDim.x) {
+      const int lt = f >> 7, kk = (f >> 5) & 3, ln = f & 31;
+      const int r = kk * 4 + (ln & 3), c = lt * 8 + (ln >> 2);
+      const int64_t row = r0 + r;
+      double wv = 0.0;
+      if (row < m) {
+        const double* zc = Zt + c * TRB + TRH + r;
+        const int il = (b - b0) * BK + r;
+        wv = es[il] * zc[-1];                 // e_{i-1} z_{i-1}
+        wv = fma(ds[il], zc[0], wv);          // + d_i z_i
+        wv = fma(es[il + 1], zc[1], wv);      // + e_i z_{i+1}
+      }
+      W[f] = wv;
+    }
+  };
+  if (b0 < b1) {
+    mbar_wait(&full[0], 0);
+    form_w(b0);
+  }
+  __syncthreads();
+  const int zr = TRH + (lane & 3), zcol = lane >> 2;
+  for (int b = b0; b < b1; ++b) {
+    // block b's DMMAs first (A from the Z box, B from W(b)); then W(b + 1) is formed while they
+    // drain through the tensor pipe; one CTA barrier per block
+    const double* Zt = ring + stage_of(b) * TILE;
+    const double* Ws = wbuf + (b & 1) * WB + lane;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const double xa = Zt[(ka * 8 + zcol) * TRB + zr + kk * 4];
+      const double xb = Zt[(kb * 8 + zcol) * TRB + zr + kk * 4];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        if (t < len) {
+          const int l = t < len1 ? la0 + t : lb0 + (t - len1);
+          dmma(acc[t], t < len1 ? xa : xb, Ws[(l * 4 + kk) * FRAG]);
+        }
+      }
+    }
+    if (b + 1 < b1) {
+      mbar_wait(&full[stage_of(b + 1)], phase_of(b + 1));
+      form_w(b + 1);
+    }
+    __syncthreads();  // W(b + 1) complete; every warp has read block b's box and W(b)
+    if (threadIdx.x == 0 && b + stages < b1) {
+      const int sb = stage_of(b);
+      mbar_arrive_expect_tx(&full[sb], TILE_BYTES);
+      tma_g2s_2d(ring + sb * TILE, &zmap, (b + stages) * BK - TRH, 0, &full[sb], pol);
+    }
+  }
+  double* slot = P + (int64_t)slice * NP * NP;
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    if (t < len) {
+      const int k = t < len1 ? ka : kb;
+      const int l = t < len1 ? la0 + t : lb0 + (t - len1);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        slot[(int64_t)(l * 8 + 2 * (lane & 3) + q) * NP + k * 8 + (lane >> 2)] = acc[t][q];
+    }
+  }
+}
+
+static bool make_tmap_z_tridiag(CUtensorMap* map, const double* Z, int64_t m, int n, int64_t ldz, int NP) {
+  if ((reinterpret_cast<uintptr_t>(Z) & 15) != 0 || (ldz & 1) != 0 || m > (int64_t)INT32_MAX) return false;
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldz * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)TRB, (cuuint32_t)NP};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(Z), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NT>
+static cudaError_t gram_tridiag_nt(int64_t m, int n, const double* d, const double* e, const double* Z,
+                                   int64_t ldz, double* P, int* g_out, cudaStream_t s, bool* done) {
+  *done = false;
+  constexpr int NCP = tri_parts(NT);
+  const int64_t nblk = zp_blocks(m);
+  int64_t nsl = num_sms() / NCP;
+  if (nsl > nblk) nsl = nblk;
+  constexpr size_t tile = (size_t)TRB * NT * 8 * 8;
+  const size_t de = (size_t)(2 * (cdiv(nblk, nsl) * BK) + 1) * 8;   // the slice's d and e
+  const size_t fixed = 256 + 2 * (size_t)NT * 4 * FRAG * 8 + de;
+  int stages = (int)((SMEM_MAX - fixed) / tile);
+  if (stages > 8) stages = 8;
+  if (stages < 2) return cudaSuccess;
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (!make_tmap_z_tridiag(&tmap, Z, m, n, ldz, NT * 8)) return cudaSuccess;  // caller takes the packed path
+  const size_t bytes = fixed + stages * tile;
+  cudaError_t err = ensure_smem_attr(reinterpret_cast<const void*>(gram_tridiag_kernel<NT>), (int)bytes);
+  if (err != cudaSuccess) return err;
+  // nblk: the packed path's block count (whole 64-row panels; the extra blocks are zero rows):
+  // the same CTA slices, so the same summation order as pack + K4'
+  *g_out = (int)nsl;
+  timing_begin(s, OQR_TIMING_K4);
+  gram_tridiag_kernel<NT><<<dim3((unsigned)nsl, NCP), 32 * tri_warps(NT), bytes, s>>>(tmap, d, e, m, (int)nblk, P,
+                                                                                      stages);
+  note_launch();
+  err = cudaGetLastError();
+  timing_end(s);
+  *done = true;
+  return err;
 }
 
 template <int NT>
@@ -1008,6 +1209,17 @@ cudaError_t launch_gram_fused(int64_t m, int64_t mr, int n, const double* A, int
   case NT:                                                                                  \
     return Zh ? gram_fused_nt<NT, true>(m, mr, A, lda, Zp, Zc, Zh, P, g_out, s, accum)       \
               : gram_fused_nt<NT, false>(m, mr, A, lda, Zp, Zc, nullptr, P, g_out, s, accum);
+    OQR_NT_CASES(OQR_CASE)
+#undef OQR_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gram_tridiag(int64_t m, int n, const double* d, const double* e, const double* Z, int64_t ldz,
+                                double* P, int* g_out, cudaStream_t s, bool* done) {
+  switch ((int)cdiv(n, 8)) {
+#define OQR_CASE(NT) \
+  case NT: return gram_tridiag_nt<NT>(m, n, d, e, Z, ldz, P, g_out, s, done);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

@@ -73,6 +73,12 @@ cudaError_t launch_pack_zw_tridiag(int64_t m, int n, const double* d, const doub
 // with mirror = true.
 cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
                                cudaStream_t s);
+// K4t: slots of the upper triangle of Z^T (T Z), T = tridiag(e, d, e), streaming the column-major
+// Z once by tensor TMA with the stencil fused in (no packed copies).  *done = false (nothing
+// launched) when Z cannot be described to TMA (16-byte alignment, even ldz): the caller then packs.
+// Reduce with mirror = true.
+cudaError_t launch_gram_tridiag(int64_t m, int n, const double* d, const double* e, const double* Z, int64_t ldz,
+                                double* P, int* g_out, cudaStream_t s, bool* done);
 // G (n x n, ldg) = sum_{c<g} P[c] in fixed c order.
 cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s,
                                bool sym = false,

@@ -102,3 +102,21 @@ def test_product_path_never_touches_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "oqr_oracle" not in src and "orc_" not in src, f
+
+
+def test_fast_path_query_without_gpu():
+    """oqr_gram_fast_path is pure host logic (no CUDA call): fast for a 16-byte aligned A with even
+    lda, slow for odd lda or an 8-byte offset, argument errors as documented in include/oqr.h."""
+    import ctypes
+    import paper_1401_5171_b200 as oqr
+    L = oqr.lib()
+    buf = (ctypes.c_double * 64)()
+    base = ctypes.addressof(buf)
+    a16 = base + ((-base) % 16)
+    assert L.oqr_gram_fast_path(4, ctypes.c_void_p(a16), 4) == 1
+    assert L.oqr_gram_fast_path(4, ctypes.c_void_p(a16), 5) == 0
+    assert L.oqr_gram_fast_path(4, ctypes.c_void_p(a16 + 8), 4) == 0
+    assert L.oqr_gram_fast_path(4, ctypes.c_void_p(a16 + 4), 4) == -3
+    assert L.oqr_gram_fast_path(4, None, 4) == -3
+    assert L.oqr_gram_fast_path(4, ctypes.c_void_p(a16), 3) == -4
+    assert L.oqr_gram_fast_path(0, ctypes.c_void_p(a16), 4) == -1

@@ -113,3 +113,30 @@ def test_eigenvector_closed_form_gpu(oqr):
 def test_full_size_config_T(oqr, variant):
     d, e, p = gen.tridiag_config("T")
     gates(oqr, d, e, p, variant, check_orth=(variant != "normal2"))
+
+
+@pytest.mark.parametrize("m,n", [(2000, 30), (1031, 1), (517, 240), (96, 96), (16, 8), (17, 9), (100000, 200)])
+def test_fused_stencil_gram_bitwise_packed_path(oqr, m, n):
+    """K4t (Z read once by tensor TMA, stencil fused, 20-row boxes with halo) against the packed path
+    (Zp and W = T Z through HBM, then K4'), which an odd ldz selects: the same W arithmetic and the
+    same DMMA schedule, so G is bitwise equal wherever both use the same K-slices -- including the
+    halo rows at block and CTA-slice boundaries and the first / last rows of T -- and within T1 of
+    the oracle everywhere."""
+    d, e = gen.tridiag(m, 1e3)
+    p = gen.problem(m, n, 1e3, 1e2, 71, with_A=False)
+    dg, eg = torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda()
+    Zev = torch.full((n, m + (m & 1)), float("nan"), dtype=torch.float64)
+    Zev[:, :m] = torch.from_numpy(p.Z)                     # even ldz (16-byte aligned): the fused path
+    Zev = Zev.cuda()
+    Zodd = torch.full((n, m + (1 if m % 2 == 0 else 2)), float("nan"), dtype=torch.float64)
+    Zodd[:, :m] = torch.from_numpy(p.Z)                    # odd ldz: the packed path
+    Zodd = Zodd.cuda()
+    G1 = oqr.gram_tridiag(dg, eg, Zev)
+    G2 = oqr.gram_tridiag(dg, eg, Zodd)
+    NT = (n + 7) // 8
+    if NT < 22 or NT > 25:   # the same K-slices on both paths (K4t runs two CTA parts per slice
+        assert torch.equal(G1, G2)   # from NT = 22, K4' from NT = 26): bitwise
+    Go = oracle.from_cm(oracle.gram_tridiag(d, e, p.Z, m), n)
+    Zd = oracle.from_cm(p.Z, m)
+    M = np.abs(Zd).T @ absT_times(d, e, Zd)
+    assert np.all(np.abs(G1.cpu().numpy().T - Go) <= 2 * gamma(m + 3) * M)
