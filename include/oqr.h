@@ -74,13 +74,15 @@ int oqr_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double*
  * caller whose A, Z live in host memory and who wants Q, R back in host memory.  A (lda >= m),
  * Z (ldz >= m) are read; Q (leading dimension m) and R (n x n, leading dimension n) are written.
  * Page-locked host memory (cudaHostAlloc / cudaHostRegister) gives full PCIe bandwidth and the
- * overlap below; pageable memory works, serialised.  The library stages A through device memory
- * from its pool in column chunks of `chunk_cols` columns (0: automatic, ~m/8; rounded up to a
- * multiple of 64) on its own copy stream, and runs the fused Gram on each chunk as soon as it has
- * landed (G = sum_J Z^T A[:, J] Z[J, :], chunks summed in order into the same per-CTA slots:
+ * overlap below; pageable memory works, serialised.  The library streams A through a ring of
+ * three device chunk buffers from its pool, `chunk_cols` columns each (0: automatic -- the ring
+ * is ~1 GiB whatever m is, at most m/8 columns a chunk; rounded up to a multiple of 64), on its
+ * own copy stream, and runs the fused Gram on each chunk as soon as it has landed
+ * (G = sum_J Z^T A[:, J] Z[J, :], chunks summed in order into the same per-CTA slots:
  * deterministic for a given chunk size, within the same T1 bound as oqr_normal but not bitwise
  * equal to it), so the A transfer -- the bound of a host-to-host factorisation -- hides all
- * but the last chunk's Gram.  Synchronous on `stream`.  Status and argument codes as oqr_normal
+ * but the last chunk's Gram, and the device footprint does not grow with A (an A larger than
+ * the GPU's memory factors).  Synchronous on `stream`.  Status and argument codes as oqr_normal
  * (-3 / -5 / -7 / -8: null host pointer), plus -9 for chunk_cols < 0.
  */
 int oqr_normal_host(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,

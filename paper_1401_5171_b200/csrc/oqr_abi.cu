@@ -311,45 +311,61 @@ static int run_normal_host(int64_t m, int n, const double* A, int64_t lda, const
   Workspace ws;
   int st = ws.alloc(m, n, s);
   if (st) return st;
+  // A moves through a ring of NBUF device chunk buffers (not a device copy of all of A): the
+  // device footprint is bounded (~1 GiB by default, whatever m is), so it stays below the pool's
+  // cache threshold and repeated calls allocate nothing.
+  constexpr int NBUF = 3;
   const int64_t ldd = m + (m & 1);
-  const size_t dbytes = ((size_t)ldd * (size_t)m + 2 * (size_t)m * (size_t)n) * sizeof(double);
+  int64_t chunk = chunk_cols;
+  if (chunk <= 0) {
+    chunk = (int64_t)((1ull << 30) / ((uint64_t)NBUF * (uint64_t)ldd * 8ull));
+    chunk = std::min<int64_t>(chunk, cdiv(m, 8));
+  }
+  chunk = std::max<int64_t>(BM, cdiv(chunk, BM) * BM);
+  const int64_t nchunks = cdiv(m, chunk);
+  const int nbuf = (int)std::min<int64_t>(NBUF, nchunks);
+  const size_t dbytes = ((size_t)ldd * (size_t)chunk * nbuf + 2 * (size_t)m * (size_t)n) * sizeof(double);
   double* buf = nullptr;
   cudaMemPool_t pool = library_pool();
   if (pool == nullptr || cudaMallocFromPoolAsync(reinterpret_cast<void**>(&buf), dbytes, pool, s) != cudaSuccess) {
     cudaGetLastError();
     return -101;
   }
-  double* Ad = buf;
-  double* Zd = Ad + (size_t)ldd * (size_t)m;
+  double* Zd = buf + (size_t)ldd * (size_t)chunk * nbuf;
   double* Qd = Zd + (size_t)m * (size_t)n;
-  int64_t chunk = chunk_cols > 0 ? chunk_cols : cdiv(m, 8);
-  chunk = cdiv(chunk, BM) * BM;
-  const int64_t nchunks = cdiv(m, chunk);
   cudaStream_t cs = nullptr;
-  std::vector<cudaEvent_t> ev((size_t)nchunks + 1, nullptr);
+  cudaEvent_t ev_start = nullptr, ev_copy[NBUF] = {}, ev_used[NBUF] = {};
   cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-  for (auto& x : ev)
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  for (int i = 0; i < NBUF && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&ev_copy[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_used[i], cudaEventDisableTiming);
+  }
   // the copy stream starts after the pool allocation (stream-ordered on s)
-  if (e == cudaSuccess) e = cudaEventRecord(ev[nchunks], s);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[nchunks], 0);
+  if (e == cudaSuccess) e = cudaEventRecord(ev_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_start, 0);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(Zd, (size_t)m * 8, Z, (size_t)ldz * 8, (size_t)m * 8, (size_t)n, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = launch_pack_z(m, n, Zd, m, ws.Zp, s);
   const int NT = (int)cdiv(n, 8);
   int g0 = 0;
   for (int64_t j = 0; j < nchunks && e == cudaSuccess; ++j) {
+    const int bi = (int)(j % nbuf);
+    double* Ab = buf + (size_t)ldd * (size_t)chunk * bi;
     const int64_t c0 = j * chunk, w = std::min(chunk, m - c0);
-    e = cudaMemcpy2DAsync(Ad + c0 * ldd, (size_t)ldd * 8, A + c0 * lda, (size_t)lda * 8, (size_t)m * 8, (size_t)w,
-                          cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[j], cs);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[j], 0);
+    // buffer bi is free once the Gram of chunk j - nbuf (recorded on s) has run
+    if (j >= nbuf) e = cudaStreamWaitEvent(cs, ev_used[bi], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(Ab, (size_t)ldd * 8, A + c0 * lda, (size_t)lda * 8, (size_t)m * 8, (size_t)w,
+                            cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_copy[bi], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_copy[bi], 0);
     int g = 0;
     // chunk columns c0.. are k-blocks of Z rows c0.. (packed blocks of 16 rows; c0 % 64 == 0);
     // the contraction operand is all of Z
     if (e == cudaSuccess)
-      e = launch_gram_fused(w, m, n, Ad + c0 * ldd, ldd, ws.Zp + (c0 / BK) * NT * 4 * FRAG, ws.Zp, nullptr, ws.P, &g,
-                            s, j > 0);
+      e = launch_gram_fused(w, m, n, Ab, ldd, ws.Zp + (c0 / BK) * NT * 4 * FRAG, ws.Zp, nullptr, ws.P, &g, s, j > 0);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_used[bi], s);
     if (j == 0) g0 = g;
   }
   if (e == cudaSuccess) e = launch_gram_reduce(n, g0, ws.P, ws.G, n, s, false);
@@ -363,8 +379,11 @@ static int run_normal_host(int64_t m, int n, const double* A, int64_t lda, const
   cudaFreeAsync(buf, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   else cudaStreamSynchronize(s);
-  for (auto& x : ev)
-    if (x) cudaEventDestroy(x);
+  if (ev_start) cudaEventDestroy(ev_start);
+  for (int i = 0; i < NBUF; ++i) {
+    if (ev_copy[i]) cudaEventDestroy(ev_copy[i]);
+    if (ev_used[i]) cudaEventDestroy(ev_used[i]);
+  }
   if (cs) cudaStreamDestroy(cs);
   if (e != cudaSuccess) return cuda_status(e);
   return info;
@@ -445,6 +464,162 @@ static AOp tridiag_op(const double* d, const double* e) {
   return op;
 }
 
+// ---- cached CUDA graphs for small synchronous calls -------------------------------------
+// A small factorisation is launch-bound (c1: 5 kernels in ~0.15 ms of which ~40 us are launch
+// gaps, the pool allocation and the status read).  The second time the same synchronous call
+// (variant, sizes, pointers, stream, device) is seen, its asynchronous form is captured once into
+// a CUDA graph with its own persistent workspace, status word and stream; that call and every
+// later identical one replays the graph: the same kernels on the same data layout, so the result
+// is bitwise the direct path's.  Only dense calls with m*m*n <= OQR_GRAPH_MAX_MMN (a large call
+// gains nothing), at most OQR_GRAPH_ENTRIES cached graphs per process (least recently used
+// evicted), never while the timing hook is on.  A call whose entry is in use by another thread,
+// or whose capture fails, takes the direct path.
+static constexpr double OQR_GRAPH_MAX_MMN = 1.1e10;
+static constexpr int OQR_GRAPH_ENTRIES = 8;
+
+struct GraphKey {
+  int which = -1, dev = -1;
+  int64_t m = 0, n = 0, lda = 0, ldz = 0;
+  const void *A = nullptr, *Z = nullptr, *Q = nullptr, *R = nullptr, *stream = nullptr;
+  bool operator==(const GraphKey& o) const {
+    return which == o.which && dev == o.dev && m == o.m && n == o.n && lda == o.lda && ldz == o.ldz && A == o.A &&
+           Z == o.Z && Q == o.Q && R == o.R && stream == o.stream;
+  }
+};
+
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  void* ws = nullptr;
+  int* d_status = nullptr;
+  int* h_status = nullptr;
+  uint64_t last = 0;
+  bool busy = false;
+  void release() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (cs) cudaStreamDestroy(cs);
+    if (ws) cudaFree(ws);
+    if (h_status) cudaFreeHost(h_status);
+    *this = GraphEntry();
+  }
+};
+
+static std::mutex g_graph_mu;
+static std::vector<GraphEntry> g_graphs;
+static std::vector<std::pair<GraphKey, bool>> g_seen;  // recent keys (bool: capture failed)
+static uint64_t g_graph_clock = 0;
+
+static int run_variant(int which, const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q,
+                       double* R, cudaStream_t s, const Async* as);
+
+// Returns 1 and *status when the call was served by a cached graph; 0 to take the direct path.
+static int graph_call(int which, const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q,
+                      double* R, cudaStream_t s, int* status) {
+  if (g_timing || (double)m * (double)m * (double)n > OQR_GRAPH_MAX_MMN) return 0;
+  GraphKey key;
+  key.which = which;
+  if (cudaGetDevice(&key.dev) != cudaSuccess) return 0;
+  key.m = m; key.n = n; key.lda = op.lda; key.ldz = ldz;
+  key.A = op.A; key.Z = Z; key.Q = Q; key.R = R; key.stream = s;
+  GraphEntry* e = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (auto& g : g_graphs)
+      if (g.exec && g.key == key) e = &g;
+    if (e) {
+      if (e->busy) return 0;
+      e->busy = true;
+      e->last = ++g_graph_clock;
+    } else {
+      auto it = std::find_if(g_seen.begin(), g_seen.end(), [&](const auto& k) { return k.first == key; });
+      if (it == g_seen.end()) {  // first sighting: remember it, run directly
+        if (g_seen.size() >= 16) g_seen.erase(g_seen.begin());
+        g_seen.push_back({key, false});
+        return 0;
+      }
+      if (it->second) return 0;  // capture failed before
+      it->second = true;         // (cleared below on success)
+      if ((int)g_graphs.size() < OQR_GRAPH_ENTRIES) g_graphs.emplace_back();
+      GraphEntry* victim = &g_graphs[0];
+      for (auto& g : g_graphs) {
+        if (!g.exec) { victim = &g; break; }
+        if (!g.busy && g.last < victim->last) victim = &g;
+      }
+      if (victim->busy) return 0;
+      victim->release();
+      victim->key = key;
+      victim->busy = true;
+      victim->last = ++g_graph_clock;
+      e = victim;
+    }
+  }
+  if (!e->exec) {  // capture the asynchronous form once
+    const size_t bytes = Workspace::doubles_for(m, n, m) * sizeof(double);
+    bool ok = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) == cudaSuccess &&
+              cudaMalloc(&e->ws, bytes) == cudaSuccess && cudaMalloc(&e->d_status, 16) == cudaSuccess &&
+              cudaHostAlloc(&e->h_status, 16, cudaHostAllocDefault) == cudaSuccess;
+    if (ok) {
+      Async as;
+      as.ws = e->ws;
+      as.bytes = bytes;
+      as.d_status = e->d_status;
+      cudaGraph_t graph = nullptr;
+      ok = cudaStreamBeginCapture(e->cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        const int st = run_variant(which, op, m, n, Z, ldz, Q, R, e->cs, &as);
+        ok = (cudaStreamEndCapture(e->cs, &graph) == cudaSuccess) && st == 0 && graph != nullptr;
+      }
+      if (ok) ok = cudaGraphInstantiate(&e->exec, graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    if (!ok) {
+      cudaGetLastError();
+      std::lock_guard<std::mutex> lock(g_graph_mu);
+      e->release();
+      return 0;
+    }
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (auto& k : g_seen)
+      if (k.first == key) k.second = false;
+  }
+  cudaError_t err = cudaEventRecord(e->ev_in, s);
+  if (err == cudaSuccess) err = cudaStreamWaitEvent(e->cs, e->ev_in, 0);
+  if (err == cudaSuccess) err = cudaGraphLaunch(e->exec, e->cs);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(e->h_status, e->d_status, sizeof(int), cudaMemcpyDeviceToHost, e->cs);
+  if (err == cudaSuccess) err = cudaEventRecord(e->ev_out, e->cs);
+  if (err == cudaSuccess) err = cudaStreamWaitEvent(s, e->ev_out, 0);   // later work on s is ordered
+  if (err == cudaSuccess) err = cudaStreamSynchronize(e->cs);
+  *status = (err == cudaSuccess) ? *e->h_status : cuda_status(err);
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  e->busy = false;
+  return 1;
+}
+
+static int run_variant(int which, const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q,
+                       double* R, cudaStream_t s, const Async* as) {
+  switch (which) {
+    case 0: return run_normal(op, m, n, Z, ldz, Q, R, s, as);
+    case 1: return run_normal2(op, m, n, Z, ldz, Q, R, s, as);
+    case 2: return run_prequr(op, m, n, Z, ldz, Q, R, s, as);
+    case 4: return run_prequr_hh(op, m, n, Z, ldz, Q, R, s, as);
+    default: return run_prequr_stable(op, m, n, Z, ldz, Q, R, s, as);
+  }
+}
+
+// The synchronous dense entry points: a cached graph when one applies, else the direct path.
+static int sync_call(int which, const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
+                     cudaStream_t s) {
+  int status = 0;
+  if (graph_call(which, op, m, n, Z, ldz, Q, R, s, &status)) return status;
+  return run_variant(which, op, m, n, Z, ldz, Q, R, s, nullptr);
+}
+
 }  // namespace oqr
 
 extern "C" {
@@ -453,14 +628,14 @@ int oqr_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double*
                double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
-  return run_normal(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(0, dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_normal2(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                 double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
-  return run_normal2(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(1, dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_normal_host(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
@@ -475,7 +650,7 @@ int oqr_prequr(int64_t m, int64_t n, const double* A, int64_t lda, const double*
                double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
-  return run_prequr(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(2, dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t oqr_workspace_bytes(int64_t m, int64_t n) {
@@ -534,7 +709,7 @@ int oqr_prequr_hh(int64_t m, int64_t n, const double* A, int64_t lda, const doub
                   double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
-  return run_prequr_hh(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(4, dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_prequr_hh_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
@@ -565,7 +740,7 @@ int oqr_prequr_stable(int64_t m, int64_t n, const double* A, int64_t lda, const 
                       double* Q, double* R, oqr_stream_t stream) {
   int st = check_args(m, n, A, lda, Z, ldz, Q, R, true, true);
   if (st) return st;
-  return run_prequr_stable(dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(3, dense_op(A, lda), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_prequr_stable_sym(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,

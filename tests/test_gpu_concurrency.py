@@ -47,9 +47,9 @@ def test_threads_on_separate_streams_bitwise():
 
 
 def test_pool_releases_host_call_staging():
-    """oqr_normal_host stages A in device memory from the library pool; a staging buffer above the
-    pool's 4 GiB release threshold is not kept reserved after the call, and
-    oqr_pool_trim(0) empties the pool."""
+    """oqr_normal_host streams A through a bounded ring of device chunk buffers from the library
+    pool (~1 GiB, not a device copy of A): after a call on a 4.6 GB A the pool holds less than A
+    (no A-sized reservation outlives the call), and oqr_pool_trim(0) empties it."""
     import numpy as np
     import paper_1401_5171_b200 as oqr
     m, n = 24000, 16                       # A = 4.6 GB > 4 GiB
@@ -63,3 +63,27 @@ def test_pool_releases_host_call_staging():
     assert oqr.pool_reserved() < m * m * 8
     oqr.pool_trim(0)
     assert oqr.pool_reserved() == 0
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_stable", "prequr_hh"])
+def test_cached_graph_calls_bitwise_direct(variant):
+    """The second identical synchronous call of a small problem is captured into a CUDA graph and
+    replayed from then on (include/oqr.h): the same kernels, so the results are bitwise the first
+    (direct) call's, also for a later call with different output buffers (a new key: direct again)."""
+    import paper_1401_5171_b200 as oqr
+    p = gen.problem(3000, 48, 1e4, 1e3, 95)
+    A, Z = torch.from_numpy(p.A).cuda(), torch.from_numpy(p.Z).cuda()
+    Q = torch.empty((48, 3000), dtype=torch.float64, device="cuda")
+    R = torch.empty((48, 48), dtype=torch.float64, device="cuda")
+    fn = oqr.VARIANTS[variant]
+    outs = []
+    for _ in range(4):                     # direct, capture + replay, replay, replay
+        Q.fill_(float("nan"))
+        R.fill_(float("nan"))
+        _, _, st = fn(A, Z, Q, R)
+        assert st == 0
+        outs.append((Q.clone(), R.clone()))
+    for Qx, Rx in outs[1:]:
+        assert torch.equal(Qx, outs[0][0]) and torch.equal(Rx, outs[0][1])
+    Q2, R2, st = fn(A, Z)                  # fresh outputs: another key
+    assert st == 0 and torch.equal(Q2, outs[0][0]) and torch.equal(R2, outs[0][1])

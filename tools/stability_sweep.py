@@ -1,7 +1,9 @@
-"""The paper's s7 stability sweep through the GPU C ABI: cases 1, 2, 3, 5,
-m = 80, n = 10, kappa(A) = 10^1..10^15, kappa(Z) = kappa(A)^{1/2}, variants normal / normal2 /
-prequr.  Errors are formed in numpy long double (80-bit; not the test oracle).  Writes a CSV and
-prints per-case slope fits of log10 ||Q^T A Q - I||_2 against log10 kappa(A).
+"""The paper's s7 stability sweep through the GPU C ABI on the paper's own
+construction (dense random V = orth(randn(m)), W = orth(randn(n)); gen.problem_haar): cases 1-5
+(case 4: random Z), m = 80, n = 10, kappa(A) = 10^1..10^15, kappa(Z) = kappa(A)^{1/2}, variants
+normal / normal2 / prequr / prequr_hh (Householder pre-step).  Errors are formed in numpy long
+double (80-bit; not the test oracle).  Writes a CSV and prints per-case slope fits of
+log10 ||Q^T A Q - I||_2 against log10 kappa(A).
 
     python tools/stability_sweep.py [out.csv]
 """
@@ -18,14 +20,15 @@ import gen  # noqa: E402
 import paper_1401_5171_b200 as oqr  # noqa: E402
 
 M, N = 80, 10
-CASES = {"case1": "bottom", "case2": "top", "case3": "split", "case5": "aorth"}
+CASES = {f"case{k}": u for k, u in gen.PAPER_CASES.items()}
+VARIANTS = ("normal", "normal2", "prequr", "prequr_hh")
 out = sys.argv[1] if len(sys.argv) > 1 else "stability_sweep.csv"
 rows = []
 for case, ucase in CASES.items():
-    for variant in ("normal", "normal2", "prequr"):
+    for variant in VARIANTS:
         for e in range(1, 16):
             ka = 10.0 ** e
-            p = gen.problem(M, N, ka, math.sqrt(ka), 7, ucase=ucase)
+            p = gen.problem_haar(M, N, ka, math.sqrt(ka), 7, ucase)
             Q, R, st = oqr.VARIANTS[variant](torch.from_numpy(p.A).cuda(), torch.from_numpy(p.Z).cuda())
             row = dict(case=case, variant=variant, kappa_A=ka, kappa_Z=math.sqrt(ka), status=st)
             if st == 0:
@@ -46,7 +49,7 @@ with open(out, "w", newline="") as f:
     for r in rows:
         w.writerow(r)
 for case in CASES:
-    for variant in ("normal", "normal2", "prequr"):
+    for variant in VARIANTS:
         rr = [r for r in rows if r["case"] == case and r["variant"] == variant and r["status"] == 0
               and r["orth"] < 1e-2]
         if len(rr) >= 3:

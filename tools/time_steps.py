@@ -30,9 +30,9 @@ if cfg in gen.TRIDIAG_CONFIGS:
 
     G = oqr.gram_tridiag(dg, eg, Z)
     R, info = oqr.potrf(G)
-    res = {"gram_tridiag (pack Z, pack TZ, K4', K1r)": timed(lambda: oqr.gram_tridiag(dg, eg, Z, G)),
+    res = {"gram_tridiag (K4t fused stencil, K1r)": timed(lambda: oqr.gram_tridiag(dg, eg, Z, G)),
            "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)), "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
-    for v in ("normal", "normal2", "prequr"):
+    for v in ("normal", "normal2", "prequr", "prequr_hh"):
         res[v] = timed(lambda: oqr.VARIANTS_TRIDIAG[v](dg, eg, Z))
     fl = 2.0 * m * n * n
     print(f"tridiag config {cfg} m={m} n={n}: " + ", ".join(f"{k} {v:.4f} ms" for k, v in res.items()) +
@@ -71,7 +71,8 @@ res = {"gram (pack+K1+K1r)": timed(lambda: oqr.gram(A, Z, G)),
        "gram_euclid (pack+K4+K1r)": timed(lambda: oqr.gram_euclid(Z, m=m)),
        "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)),
        "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
-for v in ("normal", "normal2", "prequr", "prequr_stable"):
+res["hhqr (K6)"] = timed(lambda: oqr.hhqr(Z, m=m))
+for v in ("normal", "normal2", "prequr", "prequr_stable", "prequr_hh"):
     Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
     Rv = torch.empty((n, n), dtype=torch.float64, device="cuda")
     res[v] = timed(lambda: oqr.VARIANTS[v](A, Z, Q, Rv))
