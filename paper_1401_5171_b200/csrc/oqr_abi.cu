@@ -491,7 +491,6 @@ struct GraphEntry {
   GraphKey key;
   cudaGraphExec_t exec = nullptr;
   cudaStream_t cs = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   void* ws = nullptr;
   int* d_status = nullptr;
   int* h_status = nullptr;
@@ -499,8 +498,6 @@ struct GraphEntry {
   bool busy = false;
   void release() {
     if (exec) cudaGraphExecDestroy(exec);
-    if (ev_in) cudaEventDestroy(ev_in);
-    if (ev_out) cudaEventDestroy(ev_out);
     if (cs) cudaStreamDestroy(cs);
     if (ws) cudaFree(ws);
     if (h_status) cudaFreeHost(h_status);
@@ -560,8 +557,6 @@ static int graph_call(int which, const AOp& op, int64_t m, int n, const double* 
   if (!e->exec) {  // capture the asynchronous form once
     const size_t bytes = Workspace::doubles_for(m, n, m) * sizeof(double);
     bool ok = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) == cudaSuccess &&
-              cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) == cudaSuccess &&
               cudaMalloc(&e->ws, bytes) == cudaSuccess && cudaMalloc(&e->d_status, 16) == cudaSuccess &&
               cudaHostAlloc(&e->h_status, 16, cudaHostAllocDefault) == cudaSuccess;
     if (ok) {
@@ -588,13 +583,11 @@ static int graph_call(int which, const AOp& op, int64_t m, int n, const double* 
     for (auto& k : g_seen)
       if (k.first == key) k.second = false;
   }
-  cudaError_t err = cudaEventRecord(e->ev_in, s);
-  if (err == cudaSuccess) err = cudaStreamWaitEvent(e->cs, e->ev_in, 0);
-  if (err == cudaSuccess) err = cudaGraphLaunch(e->exec, e->cs);
-  if (err == cudaSuccess) err = cudaMemcpyAsync(e->h_status, e->d_status, sizeof(int), cudaMemcpyDeviceToHost, e->cs);
-  if (err == cudaSuccess) err = cudaEventRecord(e->ev_out, e->cs);
-  if (err == cudaSuccess) err = cudaStreamWaitEvent(s, e->ev_out, 0);   // later work on s is ordered
-  if (err == cudaSuccess) err = cudaStreamSynchronize(e->cs);
+  // captured on the entry's own stream (the legacy stream cannot capture), replayed on the
+  // caller's stream (any stream can launch a graph): ordered with the caller's work as before
+  cudaError_t err = cudaGraphLaunch(e->exec, s);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(e->h_status, e->d_status, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(s);
   *status = (err == cudaSuccess) ? *e->h_status : cuda_status(err);
   std::lock_guard<std::mutex> lock(g_graph_mu);
   e->busy = false;

@@ -639,6 +639,155 @@ trsm_pair_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
   }
 }
 
+// ---- K3, column-panel form (experiment build OQR_EXP_TRSM_PANEL; measured slower) -----------
+// The same substitution, with the per-tile accumulators of a warp's 8-row block limited to one
+// panel of PW column tiles: for panel P (tiles t0 .. t0+PW-1) the contributions of the tiles
+// already solved, S[j] = sum_{kt < t0} q_kt R[kt, j], are accumulated LEFT-looking (the q_kt
+// A-fragments re-read from Q, which this warp wrote, through L1/L2) -- long independent DMMA
+// streams, PW accumulators -- and the panel itself is solved right-looking as before.  Each
+// accumulator receives its terms in the same order as in trsm_dmma_kernel (k ascending, first
+// half before second half), so the result is bitwise that kernel's.  PW accumulators instead of
+// NT free registers for more warps per SM (latency hiding) and the panel's Z is prefetched under
+// the left-looking stream.
+constexpr int KP_PW = 8;      // tiles per panel
+constexpr int KP_MAXW = 16;   // warps per CTA at most (register budget: 65536 / (16 * 32) = 128)
+
+template <int NT>
+__global__ void __launch_bounds__(KP_MAXW * 32, 1)
+trsm_panel_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q (in place)
+                  const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info) {
+  if (info != nullptr && *info != 0) return;
+  extern __shared__ __align__(16) double rsm[];
+  double* const Rt_base = rsm;
+  double* const Ri_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
+  double* const Rd_base = Ri_base + (size_t)NT * 8;
+  {
+    constexpr int TOT = NT * (NT - 1) / 2 * 64;
+    for (int e0 = threadIdx.x; e0 < TOT; e0 += 8 * blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        v[u] = 0.0;
+        if (e < TOT) {
+          const int t = e >> 6;
+          int jt = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)t)) * 0.5f);
+          while (jt * (jt - 1) / 2 > t) --jt;
+          while ((jt + 1) * jt / 2 <= t) ++jt;
+          const int kt = t - jt * (jt - 1) / 2, ln = e & 31, h = (e >> 5) & 1;
+          const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
+          if (col < n) v[u] = R[(int64_t)col * ldr + k];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < TOT) Rt_base[e] = v[u];
+      }
+    }
+    for (int e = threadIdx.x; e < NT * 64; e += blockDim.x) {
+      const int jt = e >> 6, c = (e >> 3) & 7, c2 = e & 7;
+      const int r = jt * 8 + c, col = jt * 8 + c2;
+      double v = 0.0;
+      if (c <= c2) v = (col < n) ? R[(int64_t)col * ldr + r] : (c == c2 ? 1.0 : 0.0);
+      Rd_base[e] = v;
+    }
+    for (int e = threadIdx.x; e < NT * 8; e += blockDim.x)
+      Ri_base[e] = (e < n) ? 1.0 / R[(int64_t)e * ldr + e] : 1.0;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int q4 = lane & 3, gbase = lane & ~3;
+#pragma unroll 1
+  for (int64_t r0 = ((int64_t)blockIdx.x * nw + warp) * 8; r0 < m; r0 += (int64_t)gridDim.x * nw * 8) {
+    const int64_t row = r0 + (lane >> 2);
+    const bool row_ok = row < m;
+    uint32_t Rt = (uint32_t)__cvta_generic_to_shared(Rt_base);
+    uint32_t Rd = (uint32_t)__cvta_generic_to_shared(Rd_base);
+    uint32_t Ri = (uint32_t)__cvta_generic_to_shared(Ri_base);
+    int64_t ldz_l = ldz, ldq_l = ldq;
+    int n_l = n;
+    asm volatile("" : "+r"(Rt), "+r"(Rd), "+r"(Ri), "+l"(ldz_l), "+l"(ldq_l), "+r"(n_l));
+#pragma unroll 1
+    for (int t0 = 0; t0 < NT; t0 += KP_PW) {
+      constexpr int PWC = KP_PW;
+      // this panel's Z (PW tiles, two values per lane each), in flight under the left-looking stream
+      double zq[PWC][2];
+#pragma unroll
+      for (int j = 0; j < PWC; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = (t0 + j) * 8 + 2 * q4 + e;
+          zq[j][e] = (t0 + j < NT && row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+        }
+      double S[PWC][2];
+#pragma unroll
+      for (int j = 0; j < PWC; ++j) S[j][0] = S[j][1] = 0.0;
+      // left-looking: q_kt (kt < t0) from Q -- written by this warp in earlier panels (ordered by
+      // the __syncwarp below) -- onto every tile of the panel
+      if (t0 > 0) {
+        __syncwarp();
+        const int64_t qrow = r0 + (lane >> 2);
+        const bool qok = qrow < m;
+#pragma unroll 2
+        for (int kt = 0; kt < t0; ++kt) {
+          {
+            const double a0 = qok ? Q[(int64_t)(kt * 8 + q4) * ldq_l + qrow] : 0.0;
+            const double a1 = qok ? Q[(int64_t)(kt * 8 + 4 + q4) * ldq_l + qrow] : 0.0;
+#pragma unroll
+            for (int j = 0; j < PWC; ++j)
+              if (t0 + j < NT)
+                dmma_f(S[j], a0, lds_f64(Rt + 8u * (((t0 + j) * (t0 + j - 1) / 2 + kt) * 64 + lane)));
+#pragma unroll
+            for (int j = 0; j < PWC; ++j)
+              if (t0 + j < NT)
+                dmma_f(S[j], a1, lds_f64(Rt + 8u * (((t0 + j) * (t0 + j - 1) / 2 + kt) * 64 + 32 + lane)));
+          }
+        }
+      }
+      // right-looking inside the panel
+#pragma unroll
+      for (int j = 0; j < PWC; ++j) {
+        const int jt = t0 + j;
+        if (jt < NT) {
+          double tt[8];
+          {
+            const double t0v = zq[j][0] - S[j][0], t1v = zq[j][1] - S[j][1];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              tt[2 * q] = __shfl_sync(0xffffffffu, t0v, gbase | q);
+              tt[2 * q + 1] = __shfl_sync(0xffffffffu, t1v, gbase | q);
+            }
+          }
+          double qv[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            qv[c] = tt[c] * lds_f64(Ri + 8u * (jt * 8 + c));
+#pragma unroll
+            for (int c2 = c + 1; c2 < 8; ++c2) tt[c2] = fma(-qv[c], lds_f64(Rd + 8u * ((jt * 8 + c) * 8 + c2)), tt[c2]);
+          }
+          const double a0 = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
+          const double a1 = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
+#pragma unroll
+          for (int j2 = j + 1; j2 < PWC; ++j2)
+            if (t0 + j2 < NT)
+              dmma_f(S[j2], a0, lds_f64(Rt + 8u * (((t0 + j2) * (t0 + j2 - 1) / 2 + jt) * 64 + lane)));
+#pragma unroll
+          for (int j2 = j + 1; j2 < PWC; ++j2)
+            if (t0 + j2 < NT)
+              dmma_f(S[j2], a1, lds_f64(Rt + 8u * (((t0 + j2) * (t0 + j2 - 1) / 2 + jt) * 64 + 32 + lane)));
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = jt * 8 + 2 * q4 + e;
+            const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+            if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+          }
+        }
+      }
+    }
+  }
+}
+
 static int trsm_num_sms() {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -649,6 +798,33 @@ static int trsm_num_sms() {
 template <int NT>
 static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
                            double* Q, int64_t ldq, const int* info, cudaStream_t s) {
+#ifdef OQR_EXP_TRSM_PANEL  // experiment build only: the column-panel kernel (measured slower)
+  if constexpr (NT > KP_PW) {
+    constexpr bool smem_rd = true;
+    constexpr size_t bytes = trsm_smem_doubles<NT>(smem_rd) * sizeof(double);
+    if constexpr (bytes <= (size_t)SMEM_MAX) {
+      cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(trsm_panel_kernel<NT>), (int)bytes);
+      if (e != cudaSuccess) return e;
+      // warps per CTA (<= KP_MAXW): the fewest passes over the 8-row blocks, then the fewest warps
+      const int sms = trsm_num_sms();
+      const int64_t rb = cdiv(m, 8);
+      const int64_t per = cdiv(rb, sms);
+      int best_w = KP_MAXW;
+      int64_t best = INT64_MAX;
+      for (int w = 8; w <= KP_MAXW; ++w) {
+        const int64_t cost = cdiv(per, w) * w;
+        if (cost < best) { best = cost; best_w = w; }
+      }
+      int64_t g = cdiv(rb, best_w);
+      if (g > sms) g = sms;
+      timing_begin(s, OQR_TIMING_K3);
+      trsm_panel_kernel<NT><<<(unsigned)g, best_w * 32, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
+      e = cudaGetLastError();
+      timing_end(s);
+      return e;
+    }
+  }
+#endif
 #ifdef OQR_EXP_TRSM_PAIR  // experiment build only: the warp-pair kernel (measured slower)
   if constexpr (NT >= 2 && trsm_pair_smem_bytes<NT>() <= (size_t)SMEM_MAX) {
     constexpr size_t bytes = trsm_pair_smem_bytes<NT>();
