@@ -20,7 +20,7 @@ cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample: the l
 --impl reference: the oracle itself timed as the reference arm (rank 0 only).
 --sym: the NEXT-N4 symmetric family (block-lower triangle of A; own roofline).
 --tridiag: the NEXT-N3 second workload (tridiagonal A, m = 100000, n = 200; paper normalisation
-           2mn^2; roofline on the packed Gram K4').
+           2mn^2; roofline on the tridiagonal Gram K4t).
 """
 from __future__ import annotations
 
@@ -228,7 +228,8 @@ def reference_arm(args, cfg, rank):
 def bench_tridiag(args):
     """The paper's second workload (fig.perf-tridiag): A = tridiag(e, d, e),
     m = 100000, n = 200 (gen.TRIDIAG_CONFIGS["T"]), flops normalised 2 m n^2.  Roofline on the
-    packed Gram K4' (G = Z^T (T Z) on DMMA, 2 m n^2 flops per launch), timed live by the hook."""
+    tridiagonal Gram K4t (G = Z^T (T Z) on DMMA, Z read once with the stencil fused; the dominant
+    kernel of the step), timed live by the hook."""
     import torch
     import oracle
     import paper_1401_5171_b200 as oqr
@@ -264,7 +265,7 @@ def bench_tridiag(args):
     oqr.timing_enable(False)
     k4_ms = kern["K4"][0] / max(kern["K4"][1], 1)
     NT = (n + 7) // 8
-    # K4' computes the upper triangle only (G is symmetric): its algorithmic work is the upper
+    # K4t computes the upper triangle only (G is symmetric): its algorithmic work is the upper
     # 8 x 8 tiles incl. the diagonal ones, 2 m 64 NT (NT + 1) / 2 flops
     fl_k4 = 2.0 * m * 64 * NT * (NT + 1) / 2
     achieved = fl_k4 / (k4_ms * 1e-3) / 1e12
@@ -312,7 +313,8 @@ def bench_tridiag(args):
                    "m": m, "n": n, "variant": args.variant, "flops_per_step": fl,
                    "flop_normalisation": "2mn^2 (PAPER.md:960-961)",
                    "l2": "Z = %.0f MB, packed Z and T Z = %.0f MB > L2; no flush" % (8e-6 * m * n, 128e-6 * m * NT)},
-        "roofline": {"bound": "tensor", "kernel": "gram_packed_pairs (K4'): upper triangle of G = Z^T (T Z)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "gram_tridiag (K4t, Z read once by TMA, stencil fused): upper triangle of G = Z^T (T Z)",
                      "achieved": achieved,
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
                      "traffic": traffic, "algorithmic_flops_per_launch": fl_k4, "mean_launch_ms": k4_ms,
@@ -361,7 +363,7 @@ def main():
                     help="NEXT-N4 symmetric family: block-lower triangle of A only (own roofline)")
     ap.add_argument("--tridiag", action="store_true",
                     help="NEXT-N3 second workload: A tridiagonal, m = 100000, n = 200 (paper's 2mn^2 "
-                         "normalisation, own roofline on the packed Gram K4')")
+                         "normalisation, own roofline on the tridiagonal Gram K4t)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded code path even at N = 1 (it is the default for N > 1)")
     args = ap.parse_args()
@@ -473,7 +475,7 @@ def main():
     ms_total = e0.elapsed_time(e1)
     gram_ms, gram_launches, launches = oqr.timing_read()
     other_ms = {}
-    for kname, label in (("K2", "potrf (K2)"), ("K3", "trsm (K3)"), ("K4", "packed Gram (K4')"), ("K6", "hhqr (K6)")):
+    for kname, label in (("K2", "potrf (K2)"), ("K3", "trsm (K3)"), ("K4", "packed / tridiagonal Gram (K4', K4t)"), ("K6", "hhqr (K6)")):
         kms, kl = oqr.timing_read_kernel(kname)
         if kl:
             other_ms[label] = kms / kl

@@ -6,7 +6,8 @@ import os
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LINES = ["r01_bench_c3_normal.json", "r01_bench_c3_normal_sym.json", "r01_bench_tridiag_normal.json"]
+LINES = ["r01_bench_c3_normal.json", "r01_bench_c3_normal_sym.json", "r01_bench_tridiag_normal.json",
+         "r02_bench_c3_normal.json", "r02_bench_c3_normal_sym.json", "r02_bench_tridiag_normal.json"]
 
 
 @pytest.mark.parametrize("name", LINES)
@@ -39,8 +40,9 @@ def test_bench_line_has_the_contract_keys(name):
     assert abs(d["value"] - fl / (d["ms_per_step"] * 1e-3) / 1e9) / d["value"] < 1e-6
 
 
-def test_reference_line():
-    d = json.loads(open(os.path.join(ROOT, "profiles", "r01_bench_reference.json")).read().strip().splitlines()[-1])
+@pytest.mark.parametrize("name", ["r01_bench_reference.json", "r02_bench_reference.json"])
+def test_reference_line(name):
+    d = json.loads(open(os.path.join(ROOT, "profiles", name)).read().strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
 

@@ -31,7 +31,7 @@ for d in data:
     agg[k][1] += float(d["Metric Value"])
 tot = sum(v[1] for v in agg.values())
 out = [f"# {tag} launch list: ncu --metrics gpu__time_duration.sum --clock-control none",
-       "# command: python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 (configs[3], oqr_normal)",
+       "# command: python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 (configs[3], oqr_normal; warm-up launches included)",
        "# per-launch times are cold-cache and serialised: compare SHARES, not absolutes",
        f"# {'launches':>8} {'total_ms':>10} {'mean_ms':>9} {'share':>7}  kernel"]
 for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -75,6 +75,8 @@ def dram_bytes(d):
     return sum(float(d[k][0]) * MULT[d[k][1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
 
 
+tp = os.path.join(P, "k1_traffic.json")
+prev = json.load(open(tp)) if os.path.exists(tp) else {}
 traffic = {"m": 40000, "n": 200,
            "dense": {"kernel": "gram_fused_kernel<25, dense>", "dram_bytes_per_launch": dram_bytes(d),
                      "algorithmic_bytes_per_launch": 8 * 40000 ** 2,
@@ -88,4 +90,6 @@ if os.path.exists(os.path.join(G, "k1sym_c3.ncu-rep")):
                       "dram_bytes_per_launch": dram_bytes(ds),
                       "algorithmic_bytes_per_launch": 8 * 64 * 64 * P64 * (P64 + 1) // 2,
                       "source": f"profiles/{tag}_k1sym_c3_ncu_summary.txt (ncu --set full)"}
-json.dump(traffic, open(os.path.join(P, "k1_traffic.json"), "w"), indent=1)
+elif "sym" in prev:  # keep the last symmetric-schedule capture
+    traffic["sym"] = prev["sym"]
+json.dump(traffic, open(tp, "w"), indent=1)
