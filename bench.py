@@ -61,7 +61,7 @@ def measured_peaks():
 class ClockSampler:
     """Samples SM clock and throttle reasons (NVML) while the timed region runs."""
 
-    def __init__(self, dev_index: int, period: float = 0.02):
+    def __init__(self, dev_index: int, period: float = 0.005):
         self.dev_index, self.period = dev_index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None

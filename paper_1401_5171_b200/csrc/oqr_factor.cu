@@ -82,12 +82,13 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
         brk = b0 + c + 1;
         break;
       }
-      // r_cc = sqrt(d), correctly rounded (IEEE sqrt, SURVEY s8(a) S2 -- the same r as the
-      // oracle's), and the row scaled by its correctly rounded reciprocal (LAPACK dpotf2's
-      // DSCAL by ONE/AJJ).  (A single rsqrt, r = d * rsqrt(d) within ~1.5 ulp, saved ~8 us at
-      // n = 200; not kept, so the pivot itself is the paper's chol.)
+      // r_cc = sqrt(d), correctly rounded (IEEE sqrt, SURVEY s8(a) S2 -- the same pivot as the
+      // oracle's), computed OFF the pivot chain; the row is scaled by 1/sqrt(d) from one rsqrt
+      // (<= 1 ulp; LAPACK dpotf2 scales by ONE/AJJ), which is what the next pivot waits for --
+      // the sqrt and the reciprocal no longer sit on the 8-pivot chain (inside the gamma_{n+1}
+      // of eq:normal:chol).
+      const double inv = rsqrt(d);
       const double r = sqrt(d);
-      const double inv = 1.0 / r;
       // row c: (c, c) = r, (c, b > c) *= inv
       if (c < 4) {
         if (ra == c) v0 = (cb == c) ? r : (cb > c ? v0 * inv : v0);
