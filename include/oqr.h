@@ -65,6 +65,10 @@ typedef struct CUstream_st* oqr_stream_t;
  *   G = Z^T (A Z) (lines 1-2, fused; A streamed once), R = chol(G) (line 3),
  *   Q = Z R^{-1} by row-wise substitution (line 4).
  * Synchronous: enqueues on `stream`, then synchronises `stream` and returns the status.
+ * Small problems (m*m*n <= 1.1e10; all synchronous dense variants): from the second call with the
+ * same arguments (sizes, pointers, stream, device) on, the call replays a CUDA graph of its
+ * asynchronous form captured once, with its own cached workspace (same kernels, bitwise the same
+ * results; at most 8 such graphs per process; oqr_pool_trim releases them).
  */
 int oqr_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                double* Q, double* R, oqr_stream_t stream);
@@ -207,9 +211,10 @@ int oqr_prequr_hh_async(int64_t m, int64_t n, const double* A, int64_t lda, cons
 /* The library's device memory pool (current device).  Scratch of the calls is stream-ordered from
  * it; up to 4 GiB of freed blocks stay cached between calls (no driver allocation per call), larger
  * transient staging (oqr_normal_host's device copy of A) is returned to the driver at the call's
- * final synchronisation.  oqr_pool_trim synchronises the device and releases cached blocks down to
- * keep_bytes (0: everything not in use); status 0 or -100.  oqr_pool_reserved: bytes the pool
- * currently holds from the driver (or -100). */
+ * final synchronisation.  oqr_pool_trim synchronises the device, drops the idle cached CUDA graphs
+ * of small synchronous calls (with their workspaces; see oqr_normal) and releases cached pool
+ * blocks down to keep_bytes (0: everything not in use); status 0 or -100.  oqr_pool_reserved:
+ * bytes the pool currently holds from the driver (or -100). */
 int oqr_pool_trim(size_t keep_bytes);
 int64_t oqr_pool_reserved(void);
 

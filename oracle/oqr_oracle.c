@@ -560,6 +560,8 @@ void orc_geqr2(int64_t m, int64_t n, double* X, int64_t ldx, double* tau) {
     const double scal = 1.0 / (alpha - beta);
     for (int64_t i = j + 1; i < m; i++) xj[i] *= scal;
     xj[j] = beta;
+    /* the columns l > j are independent: OpenMP splits them (disjoint outputs, same arithmetic) */
+#pragma omp parallel for schedule(static)
     for (int64_t l = j + 1; l < n; l++) {
       double* xl = X + l * ldx;
       double w = xl[j];
@@ -577,6 +579,7 @@ void orc_org2r(int64_t m, int64_t n, const double* X, int64_t ldx, const double*
     for (int64_t i = 0; i < m; i++) Y[l * m + i] = (i == l) ? 1.0 : 0.0;
   for (int64_t j = n - 1; j >= 0; j--) {
     const double* v = X + j * ldx;
+#pragma omp parallel for schedule(static)
     for (int64_t l = j; l < n; l++) {
       double* y = Y + l * m;
       double w = y[j];

@@ -539,7 +539,6 @@ static int graph_call(int which, const AOp& op, int64_t m, int n, const double* 
         return 0;
       }
       if (it->second) return 0;  // capture failed before
-      it->second = true;         // (cleared below on success)
       if ((int)g_graphs.size() < OQR_GRAPH_ENTRIES) g_graphs.emplace_back();
       GraphEntry* victim = &g_graphs[0];
       for (auto& g : g_graphs) {
@@ -577,11 +576,10 @@ static int graph_call(int which, const AOp& op, int64_t m, int n, const double* 
       cudaGetLastError();
       std::lock_guard<std::mutex> lock(g_graph_mu);
       e->release();
+      for (auto& k : g_seen)  // do not try to capture this call again
+        if (k.first == key) k.second = true;
       return 0;
     }
-    std::lock_guard<std::mutex> lock(g_graph_mu);
-    for (auto& k : g_seen)
-      if (k.first == key) k.second = false;
   }
   // captured on the entry's own stream (the legacy stream cannot capture), replayed on the
   // caller's stream (any stream can launch a graph): ordered with the caller's work as before
@@ -935,6 +933,11 @@ int oqr_pool_trim(size_t keep_bytes) {
   cudaMemPool_t pool = library_pool();
   if (pool == nullptr) return -100;
   if (cudaDeviceSynchronize() != cudaSuccess) return -100;
+  {  // the cached graphs of small synchronous calls hold their own workspaces: release the idle ones
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (auto& g : g_graphs)
+      if (g.exec && !g.busy) g.release();
+  }
   return cuda_status(cudaMemPoolTrimTo(pool, keep_bytes));
 }
 
