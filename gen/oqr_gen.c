@@ -377,14 +377,21 @@ int oqr_gen_problem_haar(int64_t m, int64_t n, double kappa_a, double kappa_z, u
     oqr_gen_logspace(n, kappa_z, s);
   }
   if (A) {
+    /* rows of V contiguous (Vt[i*m + k] = V[i, k]): the same sums, k ascending, cache-friendly */
+    double* Vt = (double*)malloc(sizeof(double) * m * m);
+    for (int64_t k = 0; k < m; k++)
+      for (int64_t i = 0; i < m; i++) Vt[i * m + k] = V[k * m + i];
 #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t j = 0; j < m; j++)
       for (int64_t i = 0; i <= j; i++) {
+        const double* vi = Vt + i * m;
+        const double* vj = Vt + j * m;
         double v = 0.0;
-        for (int64_t k = 0; k < m; k++) v += V[k * m + i] * d[k] * V[k * m + j];
+        for (int64_t k = 0; k < m; k++) v += vi[k] * d[k] * vj[k];
         A[j * lda + i] = v;
         A[i * lda + j] = v;
       }
+    free(Vt);
   }
   if (Z) {
     for (int64_t l = 0; l < n; l++)

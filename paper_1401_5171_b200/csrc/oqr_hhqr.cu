@@ -77,6 +77,7 @@ struct HhArgs {
   unsigned* flags;  // [g] per-CTA column counters: CTA c has published column t's partials (zeroed)
   int rows_per;
   int g;
+  int lookahead;    // 1: a second panel buffer in shared memory -> deferred trailing updates
 };
 
 // Grid-wide barrier among the g co-resident CTAs (cooperative launch): monotonic arrival counter.
@@ -225,8 +226,8 @@ __device__ void vtc_partials(const double* Vs, int RP, int lo, int rows, int nbp
 // (may be the same).  Warp per 4-column task, lanes over rows.
 __device__ void panel_apply(const double* Vs, int RP, int lo, int rows, const double* Ms, int ldm, int ncols,
                             const double* Cs, int64_t ldcs, double* Cd, int64_t ldcd, int64_t r0, int cbase,
-                            int lane, int wid) {
-  for (int col0 = wid * HCG; col0 < ncols; col0 += HWARPS * HCG) {
+                            int lane, int wid, int nwarps = HWARPS) {
+  for (int col0 = wid * HCG; col0 < ncols; col0 += nwarps * HCG) {
     double mm[HNB][HCG];
 #pragma unroll
     for (int aa = 0; aa < HNB; ++aa)
@@ -330,8 +331,17 @@ __global__ void __launch_bounds__(HTH, 1) hhqr_kernel(HhArgs a) {
   double* red = betas + n;                  // [HNB]
   double* rowv = red + HNB;                 // [HNB]
   double* wscr = rowv + HNB;                // [HTH]: per-warp column partials / reduce-scatter slices
+  double* Vp = wscr + HTH;                  // [HNB][RP] (look-ahead only): the previous panel's V
   unsigned epoch = 0, cstep = 0;
   int colbuf = 0;
+  // Look-ahead: the trailing update of panel p is applied at once only to panel p+1's columns; the
+  // rest is deferred and done, one chunk per column step of panel p+1, by warps 1..7 while warp 0
+  // publishes and waits for the CTAs' flags (the exchange latency hides it).  Per column the same
+  // arithmetic as the undeferred update.
+  bool pending = false;
+  int dcols = 0, dcb = 0, dlo = 0, dch = 0, dnt = 0;
+  const double* dsrc = nullptr;
+  int64_t dld = 0;
   HH_MARK(1);
 
   // ---------------------------------------------------------------- factorization ----
@@ -386,6 +396,11 @@ __global__ void __launch_bounds__(HTH, 1) hhqr_kernel(HhArgs a) {
           asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.flags + (int64_t)c * HFS), "r"(cstep) : "memory");
         HH_MARK(3);
         wait_flags(a.flags, cstep, a.g, lane);
+      } else if (pending) {
+        const int d0 = jj * dch, d1 = (int)imin(dcols, d0 + dch);
+        if (d1 > d0)
+          panel_apply(Vp, RP, dlo, rows, Ms + (HNB + d0), dnt, d1 - d0, dsrc, dld, a.X, m, r0, dcb + d0, lane, wid - 1,
+                      HWARPS - 1);
       }
       __syncthreads();
       for (int k = wid; k < nk; k += HWARPS) {
@@ -447,6 +462,13 @@ __global__ void __launch_bounds__(HTH, 1) hhqr_kernel(HhArgs a) {
       HH_MARK(5);
     }
     __syncthreads();
+    if (pending) {  // chunks the column steps did not cover (a panel narrower than HNB)
+      const int d0 = nbp * dch;
+      if (d0 < dcols)
+        panel_apply(Vp, RP, dlo, rows, Ms + (HNB + d0), dnt, dcols - d0, dsrc, dld, a.X, m, r0, dcb + d0, lane, wid);
+      pending = false;
+      __syncthreads();
+    }
     // panel done: write back, turn the panel into V (zeros above, ones on the diagonal, zero
     // columns beyond the panel)
     for (int aa = 0; aa < nbp; ++aa)
@@ -497,7 +519,22 @@ __global__ void __launch_bounds__(HTH, 1) hhqr_kernel(HhArgs a) {
       }
       __syncthreads();
       // X[i, j0 + nbp + l] = C[i, l] - sum_a V[i][a] M[a][l] for this CTA's rows i >= j0
-      panel_apply(Xs, RP, lo, rows, Ms, nt, nt, Xsrc, ldsrc, a.X, m, r0, j0 + nbp, lane, wid);
+      if (a.lookahead && nt > HNB) {
+        // now: the next panel's columns; the rest during the next panel's column steps
+        panel_apply(Xs, RP, lo, rows, Ms, nt, HNB, Xsrc, ldsrc, a.X, m, r0, j0 + nbp, lane, wid);
+        for (int e = tid; e < HNB * RP; e += HTH) Vp[e] = Xs[e];
+        pending = true;
+        dcols = nt - HNB;
+        dcb = j0 + nbp + HNB;
+        dlo = lo;
+        dnt = nt;
+        dsrc = Xsrc;
+        dld = ldsrc;
+        const int nnext = (int)imin(HNB, n - (j0 + nbp));
+        dch = (dcols + nnext - 1) / nnext;
+      } else {
+        panel_apply(Xs, RP, lo, rows, Ms, nt, nt, Xsrc, ldsrc, a.X, m, r0, j0 + nbp, lane, wid);
+      }
       __syncthreads();
     }
     HH_MARK(9);
@@ -556,7 +593,7 @@ __global__ void __launch_bounds__(HTH, 1) hhqr_kernel(HhArgs a) {
 
 // ---------------------------------------------------------------- host side ----
 struct HhPlan {
-  int g = 0, rows_per = 0;
+  int g = 0, rows_per = 0, lookahead = 0;
   size_t smem = 0;
 };
 
@@ -585,6 +622,13 @@ static HhPlan hh_plan(int64_t m, int n) {
   const int P = (n + HNB - 1) / HNB;
   pl.smem = sizeof(double) * ((size_t)HNB * rp + (size_t)HNB * (HNB + n) + (size_t)HNB * n +
                               (size_t)P * HNB * HNB + 2 * (size_t)n + 2 * HNB + HTH);
+  const size_t la = sizeof(double) * (size_t)HNB * rp;  // the look-ahead panel buffer
+#ifndef OQR_EXP_HH_NOLOOKAHEAD
+  if (pl.smem + la <= (size_t)SMEM_MAX) {
+    pl.smem += la;
+    pl.lookahead = 1;
+  }
+#endif
   return pl;
 }
 
@@ -618,6 +662,7 @@ cudaError_t launch_hhqr(int64_t m, int n, const double* Z, int64_t ldz, double* 
   a.flags = a.bar + HFS;
   a.rows_per = pl.rows_per;
   a.g = pl.g;
+  a.lookahead = pl.lookahead;
   e = cudaMemsetAsync(a.bar, 0, sizeof(unsigned) * (HFS + (size_t)pl.g * HFS), s);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
