@@ -95,6 +95,7 @@ struct Workspace {
   double* R2 = nullptr;    // n x n (R2 of normal2 / U of prequr)
   double* R3 = nullptr;    // n x n (stable pre-step: R2, R3 of the CholeskyQR2 stage)
   double* R4 = nullptr;    // n x n (stable pre-step: products)
+  double* Rimg = nullptr;  // K3's image of the last K2 factor (trsm_img_doubles), written by K2
   double* H = nullptr;     // Householder QR scratch (K6): hh_scratch_doubles(m, n)
   int* info = nullptr;
   cudaStream_t s = nullptr;
@@ -104,7 +105,8 @@ struct Workspace {
     const size_t zp = (size_t)zp_doubles(m, NP);
     const size_t zc = mr_local > 0 ? (size_t)zp_doubles(mr_local, NP) : 0;
     const size_t sl = slots_doubles(n, gram_grid(m));
-    return zp + zc + sl + 5 * (size_t)n * n + 1 + hh_doubles(m, n) + 2;  // +1 pad, +2 doubles (16 B) for info
+    const size_t img = 2 * cdiv((int64_t)trsm_img_doubles((int)cdiv(n, 8)), 2);
+    return zp + zc + sl + 5 * (size_t)n * n + 1 + img + hh_doubles(m, n) + 2;  // +1 pad, +2 doubles (16 B) for info
   }
   // user_ws: caller-provided workspace of user_bytes (no allocation: CUDA-graph capturable);
   // user_info: device status word to use instead of the workspace's own.
@@ -139,7 +141,8 @@ struct Workspace {
     R2 = R1 + nn;
     R3 = R2 + nn;
     R4 = R3 + nn;
-    H = R4 + nn + ((nn & 1) ? 1 : 0);  // 16-byte aligned
+    Rimg = R4 + nn + ((nn & 1) ? 1 : 0);  // 16-byte aligned
+    H = Rimg + 2 * cdiv((int64_t)trsm_img_doubles((int)cdiv(n, 8)), 2);
     info = user_info ? user_info : reinterpret_cast<int*>(H + hh_doubles(m, n));
     return 0;
   }
@@ -230,8 +233,12 @@ static int gram_into(const AOp& op, int64_t m, int n, const double* Z, int64_t l
 static int gram_euclid_into(int64_t m, int n, const double* Z, int64_t ldz, double* G, Workspace& ws,
                             cudaStream_t s) {
   int g = 0;
-  OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
-  OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zp, ws.P, &g, s));  // Z^T Z: upper tiles, mirrored
+  bool done = false;
+  OQR_TRY(launch_gram_euclid_box(m, n, Z, ldz, ws.P, &g, s, &done));  // K4e: Z read once, no packing
+  if (!done) {
+    OQR_TRY(launch_pack_z(m, n, Z, ldz, ws.Zp, s));
+    OQR_TRY(launch_gram_packed(m, n, ws.Zp, ws.Zp, ws.P, &g, s));  // Z^T Z: upper tiles, mirrored
+  }
   OQR_TRY(launch_gram_reduce(n, g, ws.P, G, n, s, false, true));
   return 0;
 }
@@ -242,8 +249,8 @@ static int cholqr_pass(const AOp& op, int64_t m, int n, const double* Z, int64_t
                        int info_off, Workspace& ws, cudaStream_t s) {
   int st = gram_into(op, m, n, Z, ldz, ws.G, ws, s);
   if (st) return st;
-  OQR_TRY(launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s, info_off == 0));
-  OQR_TRY(launch_trsm(m, n, Z, ldz, Rout, n, Q, m, ws.info, s));
+  OQR_TRY(launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s, info_off == 0, ws.Rimg));
+  OQR_TRY(launch_trsm(m, n, Z, ldz, Rout, n, Q, m, ws.info, s, ws.Rimg));
   return 0;
 }
 
@@ -293,8 +300,8 @@ static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t 
   if (st) return st;
   // pre-step: S = chol(Z^T Z), Y = Z S^{-1} (into Q)
   if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
-  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s)))) return st;
-  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s)))) return st;
+  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true, ws.Rimg)))) return st;
+  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s, ws.Rimg)))) return st;
   // A-stage: [Q, U] = CHOLQR(A, Y) in place; breakdown code n + k
   if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
   // R = U S
@@ -369,8 +376,8 @@ static int run_normal_host(int64_t m, int n, const double* A, int64_t lda, const
     if (j == 0) g0 = g;
   }
   if (e == cudaSuccess) e = launch_gram_reduce(n, g0, ws.P, ws.G, n, s, false);
-  if (e == cudaSuccess) e = launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true);
-  if (e == cudaSuccess) e = launch_trsm(m, n, Zd, m, ws.R1, n, Qd, m, ws.info, s);
+  if (e == cudaSuccess) e = launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true, ws.Rimg);
+  if (e == cudaSuccess) e = launch_trsm(m, n, Zd, m, ws.R1, n, Qd, m, ws.info, s, ws.Rimg);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(Q, Qd, (size_t)m * (size_t)n * 8, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(R, ws.R1, (size_t)n * (size_t)n * 8, cudaMemcpyDeviceToHost, s);
@@ -401,13 +408,13 @@ static int run_prequr_stable(const AOp& op, int64_t m, int n, const double* Z, i
   const double factor = 11.0 * ((double)m * (double)n + (double)n * (double)(n + 1)) * 0x1.0p-53;
   if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
   if ((st = cuda_status(launch_shift_diag(n, ws.G, n, factor, nullptr, s)))) return st;
-  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true)))) return st;
-  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s)))) return st;
+  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true, ws.Rimg)))) return st;
+  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s, ws.Rimg)))) return st;
   double* Rk[2] = {ws.R2, ws.R3};
   for (int pass = 0; pass < 2; ++pass) {  // CholeskyQR2 on Q1, in place
     if ((st = gram_euclid_into(m, n, Q, m, ws.G, ws, s))) return st;
-    if ((st = cuda_status(launch_potrf(n, ws.G, n, Rk[pass], n, ws.info, 0, s, false)))) return st;
-    if ((st = cuda_status(launch_trsm(m, n, Q, m, Rk[pass], n, Q, m, ws.info, s)))) return st;
+    if ((st = cuda_status(launch_potrf(n, ws.G, n, Rk[pass], n, ws.info, 0, s, false, ws.Rimg)))) return st;
+    if ((st = cuda_status(launch_trsm(m, n, Q, m, Rk[pass], n, Q, m, ws.info, s, ws.Rimg)))) return st;
   }
   if ((st = cuda_status(launch_trmm(n, ws.R3, ws.R2, ws.R4, ws.info, s)))) return st;  // R3 R2
   if ((st = cuda_status(launch_trmm(n, ws.R4, ws.R1, ws.R3, ws.info, s)))) return st;  // S = (R3 R2) R1

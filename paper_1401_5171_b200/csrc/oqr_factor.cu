@@ -27,7 +27,7 @@ __device__ __forceinline__ void dmma_c(double (&d)[2], double a, double b) {
 
 __global__ void __launch_bounds__(1024, 1)
 potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ R, int64_t ldr,
-             int* info, int info_off, bool first) {
+             int* info, int info_off, bool first, double* __restrict__ img) {
   extern __shared__ double S[];
   __shared__ int s_brk;
   if (!first && *info != 0) return;  // an earlier stage already broke down: keep its code
@@ -179,17 +179,42 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
   }
   for (int l = warp; l < n; l += nwarp)
     for (int k = lane; k < n; k += 32) R[(int64_t)l * ldr + k] = (k <= l) ? S[pk(k, l)] : 0.0;
+  if (img != nullptr) {
+    // K3's shared-memory image of R (trsm_img_*): the same values K3's prologue would stage from
+    // R -- off-diagonal tiles in B-fragment order, the reciprocals of the diagonal, the diagonal
+    // tiles -- written once here, so that every K3 CTA lands it with one bulk copy
+    const int ntri = NT * (NT - 1) / 2 * 64;
+    for (int e = tid; e < ntri; e += blockDim.x) {
+      const int t = e >> 6;
+      int jt = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)t)) * 0.5f);
+      while (jt * (jt - 1) / 2 > t) --jt;
+      while ((jt + 1) * jt / 2 <= t) ++jt;
+      const int kt = t - jt * (jt - 1) / 2, ln = e & 31, h = (e >> 5) & 1;
+      const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
+      img[e] = col < n ? S[pk(k, col)] : 0.0;
+    }
+    double* Ri = img + ntri;
+    for (int e = tid; e < NT * 8; e += blockDim.x) Ri[e] = (e < n) ? 1.0 / S[pk(e, e)] : 1.0;
+    if (trsm_img_has_rd(NT)) {
+      double* Rd = Ri + NT * 8;
+      for (int e = tid; e < NT * 64; e += blockDim.x) {
+        const int jt = e >> 6, c = (e >> 3) & 7, c2 = e & 7;
+        const int r = jt * 8 + c, col = jt * 8 + c2;
+        Rd[e] = c <= c2 ? (col < n ? S[pk(r, col)] : (c == c2 ? 1.0 : 0.0)) : 0.0;
+      }
+    }
+  }
   if (tid == 0 && first) *info = 0;
 }
 
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
-                         int info_off, cudaStream_t s, bool first) {
+                         int info_off, cudaStream_t s, bool first, double* img) {
   const int NP = 8 * ((n + 7) / 8);
   const size_t bytes = (size_t)NP * (NP + 1) / 2 * sizeof(double);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(potrf_kernel), SMEM_MAX - 1024);
   if (e != cudaSuccess) return e;
   timing_begin(s, OQR_TIMING_K2);
-  potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off, first);
+  potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off, first, img);
   note_launch();
   e = cudaGetLastError();
   timing_end(s);
@@ -268,13 +293,42 @@ constexpr size_t trsm_smem_doubles(bool with_rd) {
 template <int NT, bool SMEM_RD>
 __global__ void __launch_bounds__(trsm_threads(NT), 1)
 trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q (in place)
-                 const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info) {
+                 const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info,
+                 const double* __restrict__ img) {
   if (info != nullptr && *info != 0) return;
   extern __shared__ __align__(16) double rsm[];
   double* const Rt_base = rsm;
   double* const Ri_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
   double* const Rd_base = Ri_base + (size_t)NT * 8;
-  {
+  if (img != nullptr) {
+    // K2 wrote this CTA's shared-memory image of R: one bulk copy (SASS UBLKCP) instead of
+    // ~20k scattered L2 loads per CTA (the staging loop below: ~10% of K3 at c3)
+    __shared__ __align__(8) uint64_t bar;
+    constexpr uint32_t BYTES = (uint32_t)(trsm_img_doubles_rd(NT, SMEM_RD) * sizeof(double));
+    const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(BYTES) : "memory");
+      constexpr uint32_t CH = 32768;
+      for (uint32_t o = 0; o < BYTES; o += CH) {
+        const uint32_t len = BYTES - o < CH ? BYTES - o : CH;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(rsm) + o),
+            "l"(reinterpret_cast<const char*>(img) + o), "r"(len), "r"(sbar)
+            : "memory");
+      }
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok)
+          : "r"(sbar)
+          : "memory");
+  } else {
     // staged with 8 independent loads in flight per thread (a plain loop waits one L2 round trip
     // per element: ~7% of K3 at m = 1e5)
     constexpr int TOT = NT * (NT - 1) / 2 * 64;
@@ -798,7 +852,7 @@ static int trsm_num_sms() {
 
 template <int NT>
 static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
-                           double* Q, int64_t ldq, const int* info, cudaStream_t s) {
+                           double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img) {
 #ifdef OQR_EXP_TRSM_PANEL  // experiment build only: the column-panel kernel (measured slower)
   if constexpr (NT > KP_PW) {
     constexpr bool smem_rd = true;
@@ -851,7 +905,7 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   const int sms = trsm_num_sms();
   if (g > sms) g = sms;          // persistent: R is staged once per CTA
   timing_begin(s, OQR_TIMING_K3);
-  trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info);
+  trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info, img);
   e = cudaGetLastError();
   timing_end(s);
   return e;
@@ -862,11 +916,11 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
 
 cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
-                        double* Q, int64_t ldq, const int* info, cudaStream_t s) {
+                        double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img) {
   cudaError_t e;
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT) \
-  case NT: e = trsm_nt<NT>(m, n, Z, ldz, R, ldr, Q, ldq, info, s); break;
+  case NT: e = trsm_nt<NT>(m, n, Z, ldz, R, ldr, Q, ldq, info, s, img); break;
     OQR_TRSM_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

@@ -119,6 +119,23 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// D = A * B + D when `on` (warp-uniform), as ONE predicated instruction -- no branch around the
+// mma.sync (a branch costs a WARPSYNC and keeps the compiler from hoisting the operand loads).
+__device__ __forceinline__ void dmma_if(double (&d)[2], double a, double b, bool on) {
+#ifdef OQR_EXP_NODMMA
+  if (on) {
+    d[0] += a;
+    d[1] += b;
+  }
+  return;
+#endif
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@p mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n\t}"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b), "r"((int)on));
+}
+
 // ------------------------------------------------------------------ Z packing -------------
 // Zp[((b*NT + lt)*4 + kk)*32 + ln] = Z[b*BK + kk*4 + ln%4, lt*8 + ln/4] (zero outside Z).
 // Packing through shared memory: a CTA stages a 64-row x 32-column tile of Z (plus one halo row
@@ -662,128 +679,6 @@ gram_fused_kernel(const __grid_constant__ CUtensorMap tmap, int64_t m, int64_t m
                                      u0, u1, stages, tma_ok, alay, accum, rg, ch, lane, pol_a, pol_z);
 }
 
-// ------------------------------------------------------------------ K4' -------------------
-// Tall-skinny Gram of two packed operands: G = sum_b Xp_b^T Yp_b over 16-row blocks b, with Xp,
-// Yp in the DMMA fragment order of Zp (which is simultaneously the A-operand layout of X^T and
-// the B-operand layout of Y).  Used for the Euclidean Gram Z^T Z of the PRE-CHOLQR pre-step
-// (X = Y = Z, reading R2) and for the tridiagonal Gram Z^T (T Z) (Y = T Z, NEXT-N3); both are
-// symmetric, so only the upper triangle is formed (gram_packed_pairs_kernel below).  A CTA
-// streams its block range once (X and Y, one bulk copy each per block, mbarrier ring); warps own
-// disjoint output tiles in DMMA accumulators, so the slot of the K-slice is written once.
-template <int NT>
-__device__ __forceinline__ void packed_issue(double* dst, const double* __restrict__ Xp, const double* __restrict__ Yp,
-                                            int bn, int hl0, int NTH, uint64_t* bar, uint64_t pol, int NX = NT) {
-  const uint32_t xb = NX * 4 * FRAG * 8, yb = NTH * 4 * FRAG * 8;
-  mbar_arrive_expect_tx(bar, xb + yb);
-  bulk_g2s(dst, Xp + (int64_t)bn * NT * 4 * FRAG, xb, bar, pol);
-  if (yb) bulk_g2s(dst + NT * 4 * FRAG, Yp + ((int64_t)bn * NT + hl0) * 4 * FRAG, yb, bar, pol);
-}
-
-// K4' for a symmetric product (X^T Y, G symmetric in exact arithmetic: the Euclidean Gram Z^T Z
-// and the tridiagonal Z^T (T Z)), upper triangle only -- what K2 reads; the reduction then
-// mirrors it (launch_gram_reduce(..., mirror = true)).  Tile row i of the upper triangle holds
-// NT - i tiles, so rows i and NT-1-i together hold NT + 1: each such pair is split into two
-// warps of ceil((NT+1)/2) tiles (the first: a prefix of row i; the second: the rest of row i and
-// all of row NT-1-i), plus the middle row when NT is odd -- NT warps with equal work and no tile
-// outside the triangle.  One or two CTA parts of those warps (registers: NT <= 25 fit in one
-// CTA of 32 NT threads) x K-slices; every CTA streams its block range of Xp and Yp once.
-__host__ __device__ constexpr int pairs_parts(int NT) { return NT <= 25 ? 1 : 2; }
-__host__ __device__ constexpr int pairs_tiles(int NT) { return (NT + 2) / 2; }  // ceil((NT + 1) / 2)
-__host__ __device__ constexpr int pairs_warps(int NT) { return (NT + pairs_parts(NT) - 1) / pairs_parts(NT); }
-
-template <int NT>
-__global__ void __launch_bounds__(32 * pairs_warps(NT), 1)
-gram_packed_pairs_kernel(const double* __restrict__ Xp, const double* __restrict__ Yp, int nblk,
-                         double* __restrict__ P, int stages) {
-  constexpr int NP = NT * 8;
-  constexpr int T = pairs_tiles(NT);
-  constexpr int NW = pairs_warps(NT);
-  constexpr int STAGE = 2 * NT * 4 * FRAG;  // the block's X and Y tiles
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + 8;
-  unsigned* relcnt = reinterpret_cast<unsigned*>(empty + 8);
-  double* ring = reinterpret_cast<double*>(smem + 256);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slice = blockIdx.x, nslices = gridDim.x;
-  const int b0 = (int)((int64_t)nblk * slice / nslices), b1 = (int)((int64_t)nblk * (slice + 1) / nslices);
-  const uint64_t pol = policy_evict_first();  // Xp, Yp are streamed once
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NW);
-      relcnt[s] = 0u;
-    }
-    mbar_fence_init();
-    for (int s = 0; s < stages && b0 + s < b1; ++s)
-      packed_issue<NT>(ring + s * STAGE, Xp, Yp, b0 + s, 0, NT, &full[s], pol);
-  }
-  __syncthreads();
-  // this warp's tiles: t < len1 -> (ka, la0 + t); len1 <= t < len -> (kb, lb0 + t - len1)
-  const int g = blockIdx.y * NW + warp;  // global warp index, 0 .. NT - 1 (>= NT: ring hand-off only)
-  int ka = 0, la0 = 0, len1 = 0, kb = 0, lb0 = 0, len = 0;
-  if (g < NT) {
-    const int i = g >> 1;
-    if ((NT & 1) && g == NT - 1) {  // middle row
-      ka = i; la0 = i; len1 = len = NT - i;
-    } else if ((g & 1) == 0) {      // prefix of row i
-      ka = i; la0 = i; len1 = len = T;
-    } else {                        // rest of row i, then row NT-1-i
-      ka = i; la0 = i + T; len1 = NT - i - T;
-      kb = NT - 1 - i; lb0 = NT - 1 - i; len = len1 + i + 1;
-    }
-  }
-  double acc[T][2];
-#pragma unroll
-  for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
-  int s = 0;
-  uint32_t ph = 0;
-  for (int b = b0; b < b1; ++b) {
-    mbar_wait(&full[s], ph);
-    const double* Xs = ring + s * STAGE + lane;
-    const double* Ys = Xs + NT * 4 * FRAG;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      const double xa = Xs[(ka * 4 + kk) * FRAG];
-      const double xb = Xs[(kb * 4 + kk) * FRAG];
-#pragma unroll
-      for (int t = 0; t < T; ++t) {
-        if (t < len) {
-          const int l = t < len1 ? la0 + t : lb0 + (t - len1);
-          dmma(acc[t], t < len1 ? xa : xb, Ys[(l * 4 + kk) * FRAG]);
-        }
-      }
-    }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      mbar_arrive(&empty[s]);
-      last = (atomicAdd(&relcnt[s], 1u) % NW) == NW - 1;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && b + stages < b1) {
-      mbar_wait(&empty[s], ph);
-      if (lane == 0) packed_issue<NT>(ring + s * STAGE, Xp, Yp, b + stages, 0, NT, &full[s], pol);
-      __syncwarp();
-    }
-    if (++s == stages) {
-      s = 0;
-      ph ^= 1;
-    }
-  }
-  // C tile t: rows k*8 + lane/4, cols l*8 + 2*(lane%4) + e
-  double* slot = P + (int64_t)slice * NP * NP;
-#pragma unroll
-  for (int t = 0; t < T; ++t) {
-    if (t < len) {
-      const int k = t < len1 ? ka : kb;
-      const int l = t < len1 ? la0 + t : lb0 + (t - len1);
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        slot[(int64_t)(l * 8 + 2 * (lane & 3) + e) * NP + k * 8 + (lane >> 2)] = acc[t][e];
-    }
-  }
-}
 
 // ------------------------------------------------------------------ K1r -------------------
 // G[k, l] = sum_{c=0}^{g-1} P[c][l*NP + k], c ascending (fixed order => reproducible bits).
@@ -976,156 +871,401 @@ static cudaError_t gram_fused_nt(int64_t m, int64_t mr, const double* A, int64_t
   return e;
 }
 
-// ------------------------------------------------------------------ K4t -------------------
-// Tridiagonal Gram with the stencil fused in (NEXT-N3): the upper tiles of G = Z^T (T Z) for
-// T = tridiag(e, d, e), reading Z ONCE, straight from the caller's column-major array -- no packed
-// copies of Z and T Z through HBM.  Per 16-row block b, one 2-D tensor-TMA request lands the
-// 20 x NP box of Z starting at row 16 b - 2 (two halo rows above, two below -- the box start must be
-// 16-byte aligned, so an even row (tools/tma_halo_probe.cu: an odd start row is an illegal
-// instruction); rows outside 0..m-1 and columns >= n zero-filled) as [column][20 rows] in a ring
-// stage -- the 20-double column stride makes every DMMA fragment load bank-conflict-free.  All threads then form the block's
-// W = T Z in DMMA B-fragment order in a double-buffered shared buffer (the same arithmetic as the
-// packing kernel: w = e_{i-1} z_{i-1}; w = fma(d_i, z_i, w); w = fma(e_i, z_{i+1}, w)) -- each
-// block's W formed while the previous block's DMMAs drain, one CTA barrier per block -- and the
-// warps run the upper-tile DMMA schedule of gram_packed_pairs_kernel (same tile assignment, same
-// k order: bitwise the same slots) with the A fragments read from the Z box.
-constexpr int TRB = 20;  // rows per Z box: 2 halo rows above, the block's 16, 2 halo rows below
-constexpr int TRH = 2;   // halo rows above (the box starts at the even row 16 b - 2)
-#ifndef OQR_EXP_TRI_PARTS_FROM
-#define OQR_EXP_TRI_PARTS_FROM 22
+// ------------------------------------------------------------------ K4 family -------------
+// Upper triangle of a tall-skinny Gram that is symmetric in exact arithmetic, G = sum_b X_b^T Y_b
+// over 16-row blocks b: the Euclidean Gram Z^T Z of the PRE-CHOLQR pre-step (north_star (4),
+// reading R2; X = Y = Z) and the tridiagonal Gram Z^T (T Z) (NEXT-N3; Y = T Z).  K2 reads only the
+// upper triangle; the reduction mirrors it (launch_gram_reduce(..., mirror = true)).  Three
+// operand sources, one DMMA schedule:
+//   UPK_EUCLID  (K4e) Z read ONCE from the caller's column-major array: one 2-D tensor-TMA request
+//               per block lands the 20 x NP box of Z starting at row 16 b - 2 as [column][20 rows]
+//               (the 20-double column stride makes every A- and B-fragment load conflict-free; an
+//               even start row is what TMA requires, tools/tma_halo_probe.cu), rows outside
+//               0..m-1 and columns >= n zero-filled.  No packed copy of Z through HBM.
+//   UPK_TRI     (K4t) the same box; two producer warps form W = T Z for the block in B-fragment
+//               order in a ring of W buffers (the packing kernel's arithmetic, PAPER.md:957-961
+//               workload, reading R18) while the consumers run earlier blocks' DMMAs -- no packed Z
+//               or T Z through HBM.
+//   UPK_PACKED  (K4') Xp, Yp already packed in fragment order (the fallback when TMA cannot
+//               describe Z: odd ldz or 8-byte alignment), one bulk copy each (one when X = Y).
+// Schedule (round 2): tile rows are taken in PAIRS (2p, 2p+1); a unit is one tile column l >= 2p
+// of a pair -- two 8x8 output tiles sharing the unit's B fragment (the lower tile (2p+1, 2p) is
+// skipped).  Consumer warps own contiguous runs of at most C units (at most two pairs per warp)
+// in DMMA accumulators, so per k-step a warp loads 2-4 A fragments and one B fragment per unit
+// for up to 2 DMMAs each: about 0.6 fragment loads per DMMA instead of the one-row schedule's
+// 1.08.  One producer lane refills the ring; stages and W buffers are handed over through mbarriers
+// (full: TMA landed / W formed by every consumer; empty: every consumer warp done), no CTA barrier.
+// Each warp runs a code path compiled for its exact unit count (no predicated-off DMMA: on the
+// FP64 pipe a predicated-off DMMA still takes its issue slot).
+// The per-tile k order (blocks ascending, k-steps ascending) is the same for every source: for a
+// given K-slice split the three produce bitwise the same slots (tested).
+enum { UPK_PACKED = 0, UPK_EUCLID = 1, UPK_TRI = 2 };
+constexpr int TRB = 20;      // rows per Z box: 2 halo rows above, the block's 16, 2 halo rows below
+constexpr int TRH = 2;       // halo rows above (the box starts at the even row 16 b - 2)
+#ifndef OQR_EXP_UP_MAXC  // experiment builds only (tools/exp)
+#define OQR_EXP_UP_MAXC 6
 #endif
-// CTA parts per K-slice (two parts of half the warps each above this NT: registers)
-__host__ __device__ constexpr int tri_parts(int NT) { return NT >= OQR_EXP_TRI_PARTS_FROM ? 2 : 1; }
-__host__ __device__ constexpr int tri_warps(int NT) { return (NT + tri_parts(NT) - 1) / tri_parts(NT); }
+constexpr int UP_MAXC = OQR_EXP_UP_MAXC;  // units per consumer warp, at most (accumulators: 8 C registers)
+constexpr int UP_MAXW = 24;  // consumer warps per CTA part, at most
+__host__ __device__ constexpr int up_units(int NT) {  // sum over pairs p of (NT - 2p)
+  return ((NT + 1) / 2) * NT - ((NT + 1) / 2) * ((NT + 1) / 2 - 1);
+}
+// CTA parts per K-slice: at most 96 units per part, so that ~12 consumer warps of <= 8 units hold
+// the accumulators (8 registers per lane per unit) in ~128 registers per thread without spilling;
+// n > 144 splits the tiles over two CTA parts on two SMs, n > 208 over three
+#ifndef OQR_EXP_UP_PART_UNITS  // experiment builds only (tools/exp): units per CTA part, at most
+#define OQR_EXP_UP_PART_UNITS 96
+#endif
+#ifndef OQR_EXP_UP_WARPS       // experiment builds only: consumer warps aimed at per part
+#define OQR_EXP_UP_WARPS 16
+#endif
+__host__ __device__ constexpr int up_parts(int NT) {
+  return (up_units(NT) + OQR_EXP_UP_PART_UNITS - 1) / OQR_EXP_UP_PART_UNITS;
+}
+__host__ __device__ constexpr int up_part_units(int NT) { return (up_units(NT) + up_parts(NT) - 1) / up_parts(NT); }
+// units per warp: about 16 consumer warps per part (4 per SM sub-partition), 2..UP_MAXC units each
+__host__ __device__ constexpr int up_quota(int NT) {
+  return (up_part_units(NT) + OQR_EXP_UP_WARPS - 1) / OQR_EXP_UP_WARPS < 2
+             ? 2
+             : ((up_part_units(NT) + OQR_EXP_UP_WARPS - 1) / OQR_EXP_UP_WARPS > UP_MAXC
+                    ? UP_MAXC
+                    : (up_part_units(NT) + OQR_EXP_UP_WARPS - 1) / OQR_EXP_UP_WARPS);
+}
+// consumer warps per part, at most: the split of build_upper_sched below, counted at compile time
+// (runs of balanced length, a run cut short where it would reach a third pair)
+__host__ __device__ constexpr int up_wcap(int NT) {
+  const int U = up_units(NT), parts = up_parts(NT), q = up_quota(NT);
+  int best = 0;
+  for (int part = 0; part < parts; ++part) {
+    const int u0 = U * part / parts, u1 = U * (part + 1) / parts, nu = u1 - u0, w = (nu + q - 1) / q;
+    int u = 0, p = 0, l = 0, nw = 0, cnt = 0, segs = 0, lastp = -1, quota = 0;
+    for (p = 0, l = 0, u = 0; u < u1; ++u) {  // walk units in pair order: (p, l), l = 2p .. NT-1
+      if (u >= u0) {
+        if (nw == 0 || cnt == quota || (p != lastp && segs == 2)) {
+          quota = nu / w + (nw < nu % w ? 1 : 0);
+          quota = quota > q ? q : (quota < 1 ? 1 : quota);
+          ++nw;
+          cnt = segs = 0;
+        }
+        if (cnt == 0 || p != lastp) ++segs;
+        ++cnt;
+        lastp = p;
+      }
+      if (++l == NT) l = 2 * ++p;
+    }
+    best = nw > best ? nw : best;
+  }
+  return best;
+}
+__host__ __device__ constexpr int up_prod(int MODE) { return MODE == UPK_TRI ? 2 : 1; }  // W formers + TMA issuer
 
+// Per CTA part, per consumer warp: pa, la, l1, pb, lb, len -- units t < l1 are (pair pa, column
+// la + t), units l1 <= t < len are (pair pb, column lb + t - l1).
+struct UpperSched {
+  int nwc;  // consumer warps per CTA (the larger part; the other part's extra warps have len 0)
+  unsigned char w[4][UP_MAXW][6];
+};
+
+// Units in pair order, split into `parts` contiguous halves; each half into w = ceil(units / q)
+// runs of balanced length (floor or ceil of units / w), a run cut short where it would reach a
+// third pair.
+static bool build_upper_sched(int NT, int parts, int q, int wcap, UpperSched* S) {
+  std::memset(S, 0, sizeof(*S));
+  int up[256][2], U = 0;
+  for (int p = 0; p < (NT + 1) / 2; ++p)
+    for (int l = 2 * p; l < NT; ++l) {
+      up[U][0] = p;
+      up[U][1] = l;
+      ++U;
+    }
+  for (int part = 0; part < parts; ++part) {
+    const int u0 = U * part / parts, u1 = U * (part + 1) / parts, nu = u1 - u0;
+    const int w = (nu + q - 1) / q;
+    int nw = 0, cnt = 0, segs = 0, lastp = -1, quota = 0;
+    unsigned char* cur = nullptr;
+    for (int u = u0; u < u1; ++u) {
+      const int p = up[u][0], l = up[u][1];
+      if (cur == nullptr || cnt == quota || (p != lastp && segs == 2)) {
+        if (nw == wcap || nw == UP_MAXW) return false;
+        cur = S->w[part][nw];
+        quota = nu / w + (nw < nu % w ? 1 : 0);
+        if (quota > q) quota = q;
+        if (quota < 1) quota = 1;
+        ++nw;
+        cnt = segs = 0;
+      }
+      if (cnt == 0 || p != lastp) {
+        if (segs == 0) {
+          cur[0] = (unsigned char)p; cur[1] = (unsigned char)l;
+        }
+        cur[3] = (unsigned char)p; cur[4] = (unsigned char)l;
+        ++segs;
+      }
+      if (segs == 1) ++cur[2];
+      ++cur[5];
+      ++cnt;
+      lastp = p;
+    }
+    if (nw > S->nwc) S->nwc = nw;
+  }
+  return true;
+}
+
+// registers per thread: warps are spread over the SM's four sub-partitions, each with a quarter
+// of the register file (16384), so ceil(warps / 4) warps share one quarter
+__host__ __device__ constexpr int up_maxreg(int NT, int MODE) {
+  return (512 / ((up_prod(MODE) + up_wcap(NT) + 3) / 4)) / 8 * 8 > 248
+             ? 248
+             : (512 / ((up_prod(MODE) + up_wcap(NT) + 3) / 4)) / 8 * 8;
+}
+
+// One consumer warp's whole block loop, for a run of exactly LEN units (PRED: a run of `len` <= LEN
+// units, the DMMAs of units t >= len predicated off -- only for runs cut short at a third pair).
+// (Measured and not kept: the consumers forming W themselves, two blocks ahead, instead of two
+// producer warps -- 0.30 vs 0.24 ms at m = 1e5, n = 200.)
+struct UpShared {
+  const double* ring;
+  double* wbuf;
+  const double* ds;
+  const double* es;
+  uint64_t* zfull;
+  uint64_t* zempty;
+  uint64_t* wfull;
+  uint64_t* wempty;
+  int stages, stage, nwb, nb, b0, nwc;
+  int64_t m;
+  bool same;
+};
+
+// W(b) = T Z for block i of the slice in B-fragment order, by producer warp pw (of two): k-steps pw
+// and pw + 2, its lane the row r = 4 kk + lane%4 of every n-tile (Zt[c * TRB + TRH + r] =
+// Z[16 b + r, c], r = -2 .. 17); the three z of UPB n-tiles are loaded before any W is stored.
 template <int NT>
-__global__ void __launch_bounds__(32 * tri_warps(NT), 1)
-gram_tridiag_kernel(const __grid_constant__ CUtensorMap zmap, const double* __restrict__ d,
-                    const double* __restrict__ e, int64_t m, int nblk, double* __restrict__ P, int stages) {
+__device__ __forceinline__ void up_form_w(const UpShared& S, int i, int pw, int lane) {
+  constexpr int FB = NT * 4 * FRAG;
+  const int s = i % S.stages, j = i % S.nwb;
+  mbar_wait(&S.zfull[s], (i / S.stages) & 1);
+  if (i >= S.nwb) mbar_wait(&S.wempty[j], ((i / S.nwb) - 1) & 1);
+  const double* __restrict__ Zt = S.ring + s * S.stage;
+  double* __restrict__ W = S.wbuf + j * FB;
+  const int64_t r0 = (int64_t)(S.b0 + i) * BK;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    const int kk = pw + 2 * h;
+    const int r = kk * 4 + (lane & 3);
+    const int il = i * BK + r;
+    const bool in = r0 + r < S.m;
+    const double em = S.es[il], dd = S.ds[il], ep = S.es[il + 1];
+    const double* zc = Zt + (lane >> 2) * TRB + TRH + r;
+    double* wp = W + kk * FRAG + lane;
+    constexpr int UPB = 5;
+#pragma unroll
+    for (int l0 = 0; l0 < NT; l0 += UPB) {
+      double zm[UPB], z0[UPB], zp[UPB];
+#pragma unroll
+      for (int k = 0; k < UPB; ++k)
+        if (l0 + k < NT) {
+          const double* z = zc + (l0 + k) * 8 * TRB;
+          zm[k] = z[-1];
+          z0[k] = z[0];
+          zp[k] = z[1];
+        }
+#pragma unroll
+      for (int k = 0; k < UPB; ++k)
+        if (l0 + k < NT) {
+          double wv = em * zm[k];     // e_{i-1} z_{i-1}
+          wv = fma(dd, z0[k], wv);    // + d_i z_i
+          wv = fma(ep, zp[k], wv);    // + e_i z_{i+1}
+          wp[(l0 + k) * 4 * FRAG] = in ? wv : 0.0;
+        }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&S.wfull[j]);
+}
+
+template <int NT, int MODE, int LEN, bool PRED>
+__device__ __forceinline__ void up_consume(const UpShared& S, int cw, int lane, const unsigned char* tw,
+                                        double* __restrict__ slot) {
   constexpr int NP = NT * 8;
-  constexpr int T = pairs_tiles(NT);
-  constexpr int NW = tri_warps(NT);
-  constexpr int TILE = TRB * NP;           // doubles per Z box
-  constexpr int WB = NT * 4 * FRAG;        // doubles per W block (fragment order)
+  constexpr int FB = NT * 4 * FRAG;
+  constexpr int LA = LEN > 0 ? LEN : 1;
+  const int da = 2 * tw[0], la = tw[1], l1 = tw[2], db = 2 * tw[3], lb = tw[4], len = PRED ? tw[5] : LEN;
+  const int da1 = da + 1 < NT ? da + 1 : NT - 1, db1 = db + 1 < NT ? db + 1 : NT - 1;
+  // fragment offsets in the stage (k-step kk adds kk * AK / BKS):
+  //   packed:  A tile row k: (k*4 + kk)*FRAG + lane          B tile column l: (l*4 + kk)*FRAG + lane
+  //   Z box:   A tile row k: (k*8 + lane/4)*TRB + TRH + lane%4 + kk*4   (Z^T: lane row = Z column)
+  //            B tile column l: the same with l (lane row lane%4 = Z row, col lane/4 = Z column)
+  constexpr int AT = MODE == UPK_PACKED ? 4 * FRAG : 8 * TRB;  // per tile row of A
+  constexpr int AK = MODE == UPK_PACKED ? FRAG : 4;             // per k-step of A
+  constexpr int BT = MODE == UPK_EUCLID ? 8 * TRB : 4 * FRAG;   // per tile column of B
+  constexpr int BKS = MODE == UPK_EUCLID ? 4 : FRAG;            // per k-step of B
+  const int alane = MODE == UPK_PACKED ? lane : (lane >> 2) * TRB + TRH + (lane & 3);
+  const int blane = MODE == UPK_EUCLID ? (lane >> 2) * TRB + TRH + (lane & 3) : lane;
+  const int oa0 = da * AT + alane, oa1 = da1 * AT + alane, oc0 = db * AT + alane, oc1 = db1 * AT + alane;
+  const int ob0 = la * BT + blane, ob1 = (lb - l1) * BT + blane;  // unit t: (t < l1 ? ob0 : ob1) + t*BT
+  const int th0 = da - la, th1 = db - lb + l1;                   // second tile of unit t iff t > th
+  double acc[LA][2][2];
+#pragma unroll
+  for (int t = 0; t < LA; ++t) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.0;
+  for (int i = 0; i < S.nb; ++i) {
+    const int s = i % S.stages, j = MODE == UPK_TRI ? i % S.nwb : 0;
+    mbar_wait(&S.zfull[s], (i / S.stages) & 1);
+    if (MODE == UPK_TRI) mbar_wait(&S.wfull[j], (i / S.nwb) & 1);
+    const double* As = S.ring + s * S.stage;
+    const double* Bs = MODE == UPK_TRI ? S.wbuf + j * FB : (MODE == UPK_PACKED && !S.same ? As + FB : As);
+#ifndef OQR_EXP_K4_NOCONSUME  // experiment build only: the consumers only hand the stages back
+    if (LEN > 0) {
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        // every operand of the k-step first, then its DMMAs
+        const double a0 = As[oa0 + kk * AK], a1 = As[oa1 + kk * AK];
+        const double c0 = As[oc0 + kk * AK], c1 = As[oc1 + kk * AK];
+        double bv[LA];
+#pragma unroll
+        for (int t = 0; t < LA; ++t)
+          bv[t] = Bs[(!PRED || t < len ? (t < l1 ? ob0 : ob1) + t * BT : ob0) + kk * BKS];
+#pragma unroll
+        for (int t = 0; t < LA; ++t) {
+          const bool s0 = t < l1;
+          const bool on = !PRED || t < len;
+          dmma_if(acc[t][0], s0 ? a0 : c0, bv[t], on);                          // tile (dr, l)
+          dmma_if(acc[t][1], s0 ? a1 : c1, bv[t], on && t > (s0 ? th0 : th1));  // (dr + 1, l) iff l > dr
+        }
+      }
+    }
+#endif
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&S.zempty[s]);
+      if (MODE == UPK_TRI) mbar_arrive(&S.wempty[j]);
+    }
+  }
+  // C tile (k, l): rows k*8 + lane/4, cols l*8 + 2*(lane%4) + q
+#pragma unroll
+  for (int t = 0; t < LA; ++t) {
+    if (t < len) {
+      const bool s0 = t < l1;
+      const int l = s0 ? la + t : lb + (t - l1);
+      const int dr = s0 ? da : db;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && l <= dr) break;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          slot[(int64_t)(l * 8 + 2 * (lane & 3) + q) * NP + (dr + h) * 8 + (lane >> 2)] = acc[t][h][q];
+      }
+    }
+  }
+}
+
+template <int NT, int MODE>
+__global__ void __maxnreg__(up_maxreg(NT, MODE))
+gram_upper_kernel(const __grid_constant__ CUtensorMap zmap, const double* __restrict__ Xp,
+                  const double* __restrict__ Yp, const double* __restrict__ d, const double* __restrict__ e,
+                  int64_t m, int nblk, double* __restrict__ P, int stages, int nwb,
+                  const __grid_constant__ UpperSched sched) {
+  constexpr int NP = NT * 8;
+  constexpr int C = up_quota(NT);
+  constexpr int NPR = up_prod(MODE);
+  constexpr int FB = NT * 4 * FRAG;  // doubles per packed block operand (and per W buffer)
   extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  double* wbuf = reinterpret_cast<double*>(smem + 256);   // [2][WB]
-  double* ring = wbuf + 2 * WB;                           // [stages][TILE]
+  UpShared S;
+  S.same = MODE == UPK_PACKED && Xp == Yp;
+  S.stage = MODE == UPK_PACKED ? (S.same ? FB : 2 * FB) : TRB * NP;
+  S.zfull = reinterpret_cast<uint64_t*>(smem);
+  S.zempty = S.zfull + 8;
+  S.wfull = S.zempty + 8;
+  S.wempty = S.wfull + 4;
+  S.wbuf = reinterpret_cast<double*>(smem + 256);  // [nwb][FB] (UPK_TRI)
+  double* ring = S.wbuf + (MODE == UPK_TRI ? nwb * FB : 0);
+  S.ring = ring;
+  S.stages = stages;
+  S.nwb = nwb;
+  S.m = m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  S.nwc = sched.nwc;
   const int slice = blockIdx.x, nslices = gridDim.x;
   const int b0 = (int)((int64_t)nblk * slice / nslices), b1 = (int)((int64_t)nblk * (slice + 1) / nslices);
-  const uint64_t pol = policy_evict_first();  // Z is streamed once
-  constexpr uint32_t TILE_BYTES = TILE * 8;
-  // this slice's diagonal and the couplings of its rows (and the row above), staged once so that
-  // forming W is shared-memory only: ds[i] = d_{16 b0 + i}, es[i] = e_{16 b0 + i - 1} (0 outside)
-  double* ds = ring + stages * TILE;
-  double* es = ds + (b1 - b0) * BK;
-  {
+  S.b0 = b0;
+  S.nb = b1 - b0;
+  const uint64_t pol = policy_evict_first();  // every operand is streamed once
+  // UPK_TRI: the slice's diagonal and couplings, staged once: ds[i] = d_{16 b0 + i},
+  // es[i] = e_{16 b0 + i - 1} (0 outside)
+  double* ds = ring + stages * S.stage;
+  double* es = ds + S.nb * BK;
+  S.ds = ds;
+  S.es = es;
+  if (MODE == UPK_TRI) {
     const int64_t rs = (int64_t)b0 * BK;
-    const int nr = (b1 - b0) * BK;
+    const int nr = S.nb * BK;
     for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
       const int64_t row = rs + i;
       if (i < nr) ds[i] = row < m ? __ldg(d + row) : 0.0;
       es[i] = (row >= 1 && row - 1 < m - 1) ? __ldg(e + row - 1) : 0.0;
     }
   }
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-    for (int s = 0; s < stages && b0 + s < b1; ++s) {
-      mbar_arrive_expect_tx(&full[s], TILE_BYTES);
-      tma_g2s_2d(ring + s * TILE, &zmap, (b0 + s) * BK - TRH, 0, &full[s], pol);
-    }
-  }
-  __syncthreads();
-  const int g = blockIdx.y * NW + warp;
-  int ka = 0, la0 = 0, len1 = 0, kb = 0, lb0 = 0, len = 0;
-  if (g < NT) {
-    const int i = g >> 1;
-    if ((NT & 1) && g == NT - 1) {
-      ka = i; la0 = i; len1 = len = NT - i;
-    } else if ((g & 1) == 0) {
-      ka = i; la0 = i; len1 = len = T;
+  auto issue = [&](int b, int s) {  // block b into ring stage s
+    double* dst = ring + s * S.stage;
+    if (MODE == UPK_PACKED) {
+      const uint32_t fb = FB * 8;
+      mbar_arrive_expect_tx(&S.zfull[s], S.same ? fb : 2 * fb);
+      bulk_g2s(dst, Xp + (int64_t)b * FB, fb, &S.zfull[s], pol);
+      if (!S.same) bulk_g2s(dst + FB, Yp + (int64_t)b * FB, fb, &S.zfull[s], pol);
     } else {
-      ka = i; la0 = i + T; len1 = NT - i - T;
-      kb = NT - 1 - i; lb0 = NT - 1 - i; len = len1 + i + 1;
-    }
-  }
-  double acc[T][2];
-#pragma unroll
-  for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
-  // block b lives in stage (b - b0) % stages, phase ((b - b0) / stages) & 1
-  auto stage_of = [&](int b) { return (b - b0) % stages; };
-  auto phase_of = [&](int b) { return (uint32_t)(((b - b0) / stages) & 1); };
-  // W(b) = T Z on block b's rows, in B-fragment order, by all threads (Zt[c * TRB + TRH + r] =
-  // Z[16 b + r, c], r = -2 .. 17)
-  auto form_w = [&](int b) {
-    const double* Zt = ring + stage_of(b) * TILE;
-    double* W = wbuf + (b & 1) * WB;
-    const int64_t r0 = (int64_t)b * BK;
-    for (int f = threadIdx.x; f < WB; f += blockDim.x) {
-      const int lt = f >> 7, kk = (f >> 5) & 3, ln = f & 31;
-      const int r = kk * 4 + (ln & 3), c = lt * 8 + (ln >> 2);
-      const int64_t row = r0 + r;
-      double wv = 0.0;
-      if (row < m) {
-        const double* zc = Zt + c * TRB + TRH + r;
-        const int il = (b - b0) * BK + r;
-        wv = es[il] * zc[-1];                 // e_{i-1} z_{i-1}
-        wv = fma(ds[il], zc[0], wv);          // + d_i z_i
-        wv = fma(es[il + 1], zc[1], wv);      // + e_i z_{i+1}
-      }
-      W[f] = wv;
+      mbar_arrive_expect_tx(&S.zfull[s], (uint32_t)(TRB * NP * 8));
+      tma_g2s_2d(dst, &zmap, b * BK - TRH, 0, &S.zfull[s], pol);
     }
   };
-  if (b0 < b1) {
-    mbar_wait(&full[0], 0);
-    form_w(b0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&S.zfull[s], 1);
+      mbar_init(&S.zempty[s], S.nwc);
+    }
+    for (int j = 0; j < nwb; ++j) {
+      mbar_init(&S.wfull[j], NPR);
+      mbar_init(&S.wempty[j], S.nwc);
+    }
+    mbar_fence_init();
+    for (int s = 0; s < stages && s < S.nb; ++s) issue(b0 + s, s);
   }
   __syncthreads();
-  const int zr = TRH + (lane & 3), zcol = lane >> 2;
-  for (int b = b0; b < b1; ++b) {
-    // block b's DMMAs first (A from the Z box, B from W(b)); then W(b + 1) is formed while they
-    // drain through the tensor pipe; one CTA barrier per block
-    const double* Zt = ring + stage_of(b) * TILE;
-    const double* Ws = wbuf + (b & 1) * WB + lane;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      const double xa = Zt[(ka * 8 + zcol) * TRB + zr + kk * 4];
-      const double xb = Zt[(kb * 8 + zcol) * TRB + zr + kk * 4];
-#pragma unroll
-      for (int t = 0; t < T; ++t) {
-        if (t < len) {
-          const int l = t < len1 ? la0 + t : lb0 + (t - len1);
-          dmma(acc[t], t < len1 ? xa : xb, Ws[(l * 4 + kk) * FRAG]);
+  if (warp < NPR) {
+    if constexpr (MODE != UPK_TRI) {  // producer: the ring refills (one elected lane)
+      if (lane == 0)
+        for (int i = stages; i < S.nb; ++i) {
+          const int s = i % stages;
+          mbar_wait(&S.zempty[s], ((i / stages) - 1) & 1);
+          issue(b0 + i, s);
+        }
+    } else {  // two producer warps form W; warp 0's lane 0 also refills the ring one block behind
+      for (int i = 0; i < S.nb; ++i) {
+        up_form_w<NT>(S, i, warp, lane);
+        if (warp == 0 && lane == 0 && i >= 1 && i - 1 + stages < S.nb) {
+          const int ip = i - 1;
+          mbar_wait(&S.zempty[ip % stages], (ip / stages) & 1);
+          issue(b0 + ip + stages, ip % stages);
         }
       }
     }
-    if (b + 1 < b1) {
-      mbar_wait(&full[stage_of(b + 1)], phase_of(b + 1));
-      form_w(b + 1);
-    }
-    __syncthreads();  // W(b + 1) complete; every warp has read block b's box and W(b)
-    if (threadIdx.x == 0 && b + stages < b1) {
-      const int sb = stage_of(b);
-      mbar_arrive_expect_tx(&full[sb], TILE_BYTES);
-      tma_g2s_2d(ring + sb * TILE, &zmap, (b + stages) * BK - TRH, 0, &full[sb], pol);
-    }
+    return;
   }
+  const int cw = warp - NPR;
+  const unsigned char* tw = sched.w[blockIdx.y][cw];
   double* slot = P + (int64_t)slice * NP * NP;
-#pragma unroll
-  for (int t = 0; t < T; ++t) {
-    if (t < len) {
-      const int k = t < len1 ? ka : kb;
-      const int l = t < len1 ? la0 + t : lb0 + (t - len1);
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        slot[(int64_t)(l * 8 + 2 * (lane & 3) + q) * NP + k * 8 + (lane >> 2)] = acc[t][q];
-    }
-  }
+  const int len = tw[5];
+  if (len == C)
+    up_consume<NT, MODE, C, false>(S, cw, lane, tw, slot);
+  else if (C > 1 && len == C - 1)
+    up_consume<NT, MODE, (C > 1 ? C - 1 : 1), false>(S, cw, lane, tw, slot);
+  else if (len == 0)
+    up_consume<NT, MODE, 0, false>(S, cw, lane, tw, slot);
+  else
+    up_consume<NT, MODE, C, true>(S, cw, lane, tw, slot);
 }
 
-static bool make_tmap_z_tridiag(CUtensorMap* map, const double* Z, int64_t m, int n, int64_t ldz, int NP) {
+// The Z box map of K4e / K4t: the caller's column-major Z (m x n, ldz), box TRB rows x NP columns.
+static bool make_tmap_z_box(CUtensorMap* map, const double* Z, int64_t m, int n, int64_t ldz, int NP) {
   if ((reinterpret_cast<uintptr_t>(Z) & 15) != 0 || (ldz & 1) != 0 || m > (int64_t)INT32_MAX) return false;
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
@@ -1138,62 +1278,51 @@ static bool make_tmap_z_tridiag(CUtensorMap* map, const double* Z, int64_t m, in
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NT>
-static cudaError_t gram_tridiag_nt(int64_t m, int n, const double* d, const double* e, const double* Z,
-                                   int64_t ldz, double* P, int* g_out, cudaStream_t s, bool* done) {
+// Launch the K4 family (MODE) for NT = ceil(n/8).  *done = false (nothing launched, no error) when
+// the box modes cannot describe Z to TMA or the ring does not fit: the caller then packs.
+template <int NT, int MODE>
+static cudaError_t gram_upper_nt(int64_t m, int n, const double* Z, int64_t ldz, const double* Xp,
+                                 const double* Yp, const double* d, const double* e, double* P, int* g_out,
+                                 cudaStream_t s, bool* done) {
   *done = false;
-  constexpr int NCP = tri_parts(NT);
+  constexpr int NCP = up_parts(NT);
+  UpperSched sched;
+  if (!build_upper_sched(NT, NCP, up_quota(NT), up_wcap(NT), &sched)) return cudaErrorInvalidConfiguration;
   const int64_t nblk = zp_blocks(m);
   int64_t nsl = num_sms() / NCP;
   if (nsl > nblk) nsl = nblk;
-  constexpr size_t tile = (size_t)TRB * NT * 8 * 8;
-  const size_t de = (size_t)(2 * (cdiv(nblk, nsl) * BK) + 1) * 8;   // the slice's d and e
-  const size_t fixed = 256 + 2 * (size_t)NT * 4 * FRAG * 8 + de;
-  int stages = (int)((SMEM_MAX - fixed) / tile);
+  constexpr size_t fb = (size_t)NT * 4 * FRAG * 8;
+  const size_t stage = MODE == UPK_PACKED ? (Xp == Yp ? fb : 2 * fb) : (size_t)TRB * NT * 8 * 8;
+  const size_t de = MODE == UPK_TRI ? (size_t)(2 * (cdiv(nblk, nsl) * BK) + 1) * 8 : 0;
+  int nwb = MODE == UPK_TRI ? 3 : 0;
+  int stages = (int)((SMEM_MAX - 256 - nwb * fb - de) / stage);
+  if (MODE == UPK_TRI && stages < 3) {
+    nwb = 2;
+    stages = (int)((SMEM_MAX - 256 - nwb * fb - de) / stage);
+  }
   if (stages > 8) stages = 8;
-  if (stages < 2) return cudaSuccess;
+#ifdef OQR_EXP_K4_STAGES  // experiment build only
+  if (stages > OQR_EXP_K4_STAGES) stages = OQR_EXP_K4_STAGES;
+#endif
+  if (stages < 2) {
+    if (MODE == UPK_PACKED) return cudaErrorInvalidConfiguration;
+    return cudaSuccess;
+  }
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  if (!make_tmap_z_tridiag(&tmap, Z, m, n, ldz, NT * 8)) return cudaSuccess;  // caller takes the packed path
-  const size_t bytes = fixed + stages * tile;
-  cudaError_t err = ensure_smem_attr(reinterpret_cast<const void*>(gram_tridiag_kernel<NT>), (int)bytes);
+  if (MODE != UPK_PACKED && !make_tmap_z_box(&tmap, Z, m, n, ldz, NT * 8)) return cudaSuccess;
+  const size_t bytes = 256 + nwb * fb + de + stages * stage;
+  cudaError_t err = ensure_smem_attr(reinterpret_cast<const void*>(gram_upper_kernel<NT, MODE>), (int)bytes);
   if (err != cudaSuccess) return err;
-  // nblk: the packed path's block count (whole 64-row panels; the extra blocks are zero rows):
-  // the same CTA slices, so the same summation order as pack + K4'
   *g_out = (int)nsl;
   timing_begin(s, OQR_TIMING_K4);
-  gram_tridiag_kernel<NT><<<dim3((unsigned)nsl, NCP), 32 * tri_warps(NT), bytes, s>>>(tmap, d, e, m, (int)nblk, P,
-                                                                                      stages);
+  gram_upper_kernel<NT, MODE><<<dim3((unsigned)nsl, NCP), 32 * (up_prod(MODE) + sched.nwc), bytes, s>>>(
+      tmap, Xp, Yp, d, e, m, (int)nblk, P, stages, nwb, sched);
   note_launch();
   err = cudaGetLastError();
   timing_end(s);
   *done = true;
   return err;
-}
-
-template <int NT>
-static cudaError_t gram_packed_upper_nt(int64_t m, const double* Xp, const double* Yp, double* P, int* g_out,
-                                        cudaStream_t s) {
-  constexpr int NCP = pairs_parts(NT);
-  const size_t stage = (size_t)2 * NT * 4 * FRAG * 8;
-  int stages = (int)((SMEM_MAX - 256) / stage);
-  if (stages > 8) stages = 8;
-  const size_t bytes = 256 + stages * stage;
-  {
-    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_packed_pairs_kernel<NT>), (int)bytes);
-    if (e != cudaSuccess) return e;
-  }
-  const int64_t nblk = zp_blocks(m);
-  int64_t nsl = num_sms() / NCP;
-  if (nsl > nblk) nsl = nblk;
-  *g_out = (int)nsl;
-  timing_begin(s, OQR_TIMING_K4);
-  gram_packed_pairs_kernel<NT><<<dim3((unsigned)nsl, NCP), 32 * pairs_warps(NT), bytes, s>>>(Xp, Yp, (int)nblk, P,
-                                                                                           stages);
-  note_launch();
-  cudaError_t e = cudaGetLastError();
-  timing_end(s);
-  return e;
 }
 
 #define OQR_NT_CASES(X) \
@@ -1219,7 +1348,18 @@ cudaError_t launch_gram_tridiag(int64_t m, int n, const double* d, const double*
                                 double* P, int* g_out, cudaStream_t s, bool* done) {
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT) \
-  case NT: return gram_tridiag_nt<NT>(m, n, d, e, Z, ldz, P, g_out, s, done);
+  case NT: return gram_upper_nt<NT, UPK_TRI>(m, n, Z, ldz, nullptr, nullptr, d, e, P, g_out, s, done);
+    OQR_NT_CASES(OQR_CASE)
+#undef OQR_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gram_euclid_box(int64_t m, int n, const double* Z, int64_t ldz, double* P, int* g_out,
+                                   cudaStream_t s, bool* done) {
+  switch ((int)cdiv(n, 8)) {
+#define OQR_CASE(NT) \
+  case NT: return gram_upper_nt<NT, UPK_EUCLID>(m, n, Z, ldz, nullptr, nullptr, nullptr, nullptr, P, g_out, s, done);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;
@@ -1228,9 +1368,10 @@ cudaError_t launch_gram_tridiag(int64_t m, int n, const double* d, const double*
 
 cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double* Yp, double* P, int* g_out,
                                cudaStream_t s) {
+  bool done = false;
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT) \
-  case NT: return gram_packed_upper_nt<NT>(m, Xp, Yp, P, g_out, s);
+  case NT: return gram_upper_nt<NT, UPK_PACKED>(m, n, nullptr, 0, Xp, Yp, nullptr, nullptr, P, g_out, s, &done);
     OQR_NT_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

@@ -79,19 +79,35 @@ cudaError_t launch_gram_packed(int64_t m, int n, const double* Xp, const double*
 // Reduce with mirror = true.
 cudaError_t launch_gram_tridiag(int64_t m, int n, const double* d, const double* e, const double* Z, int64_t ldz,
                                 double* P, int* g_out, cudaStream_t s, bool* done);
+// K4e: slots of the upper triangle of Z^T Z streaming the column-major Z once by tensor TMA (no
+// packed copy).  *done = false (nothing launched) when TMA cannot describe Z: the caller packs and
+// takes launch_gram_packed (bitwise the same slots).  Reduce with mirror = true.
+cudaError_t launch_gram_euclid_box(int64_t m, int n, const double* Z, int64_t ldz, double* P, int* g_out,
+                                   cudaStream_t s, bool* done);
 // G (n x n, ldg) = sum_{c<g} P[c] in fixed c order.
 cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t ldg, cudaStream_t s,
                                bool sym = false,
                                bool mirror = false);
+// K3's shared-memory image of R, in this order: the strictly upper 8x8 tiles in DMMA B-fragment
+// order (NT(NT-1)/2 * 64 doubles), the reciprocals of the diagonal (NT * 8; 1 beyond n), the
+// diagonal tiles (NT * 64; only when the whole image fits in shared memory, NT <= 29).
+__host__ __device__ constexpr size_t trsm_img_doubles_rd(int NT, bool rd) {
+  return (size_t)NT * (NT - 1) / 2 * 64 + (size_t)NT * 8 + (rd ? (size_t)NT * 64 : 0);
+}
+__host__ __device__ constexpr bool trsm_img_has_rd(int NT) { return trsm_img_doubles_rd(NT, true) * 8 <= (size_t)SMEM_MAX; }
+__host__ __device__ constexpr size_t trsm_img_doubles(int NT) { return trsm_img_doubles_rd(NT, trsm_img_has_rd(NT)); }
 // R = chol(G) (upper).  first: *info = 0 on success, info_off + k on breakdown.  !first: does
 // nothing if *info != 0 already (an earlier stage broke down), else writes info_off + k on breakdown.
+// img != nullptr: also write K3's image of R there (trsm_img_doubles(ceil(n/8)) doubles, 16-byte
+// aligned) for a launch_trsm with the same R.
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
-                         int info_off, cudaStream_t s, bool first = true);
+                         int info_off, cudaStream_t s, bool first = true, double* img = nullptr);
 // G += factor * tr(G) * I (skipped when *info != 0).
 cudaError_t launch_shift_diag(int n, double* G, int64_t ldg, double factor, const int* info, cudaStream_t s);
-// Q = Z R^{-1}; skipped when info != nullptr && *info != 0.
+// Q = Z R^{-1}; skipped when info != nullptr && *info != 0.  img: the image launch_potrf wrote for
+// this R (each CTA lands it with one bulk copy), or nullptr (each CTA stages it from R).
 cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
-                        double* Q, int64_t ldq, const int* info, cudaStream_t s);
+                        double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img = nullptr);
 // R = R2 * R1 (upper x upper); skipped when *info != 0.
 cudaError_t launch_trmm(int n, const double* R2, const double* R1, double* R, const int* info,
                         cudaStream_t s);

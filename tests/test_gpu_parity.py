@@ -610,10 +610,11 @@ def test_normal_host_argument_errors(oqr):
     assert L.oqr_normal_host(64, 65, P(A), 64, P(Z), 64, P(Q), P(R), 0, s) == -2
 
 
-# K4' upper-triangle variant: its column parts change at NT = 6 (2 parts) and NT = 12 (4 parts);
+# K4 family (upper triangle by tile-row pairs): one CTA part per K-slice up to NT = 18, two from
+# NT = 19 (n > 144), three from NT = 27 (n > 208); quotas of 2..8 units per warp change with NT.
 # n on both sides of those boundaries and of the widest shapes, Euclidean and tridiagonal Grams
 # (T1; the mirrored lower triangle must equal the upper bitwise).
-@pytest.mark.parametrize("n", [40, 41, 48, 49, 88, 89, 96, 97, 232, 233])
+@pytest.mark.parametrize("n", [40, 41, 48, 49, 88, 89, 96, 97, 144, 145, 208, 209, 232, 233, 240])
 def test_t1_packed_upper_gram_part_boundaries(oqr, n):
     m = 1000 + n
     p = make(m, n, 1e2, 1e2, 70 + n)
@@ -630,6 +631,29 @@ def test_t1_packed_upper_gram_part_boundaries(oqr, n):
     Td = np.abs(np.diag(d)) + np.abs(np.diag(e, 1)) + np.abs(np.diag(e, -1))
     Mt = np.abs(Zd).T @ (Td @ np.abs(Zd))
     assert np.all(np.abs(Gt - Got) <= 2 * gamma(m + 3) * Mt)
+
+
+@pytest.mark.parametrize("m,n", [(1000, 1), (1031, 9), (517, 50), (3001, 145), (2003, 200), (2003, 209),
+                                 (777, 240), (40000, 200)])
+def test_euclid_box_gram_bitwise_packed_path(oqr, m, n):
+    """K4e (the Euclidean Gram reading the column-major Z once by tensor TMA, 20-row boxes) against
+    the packed path an odd ldz selects (Zp through HBM, then K4'): the same products in the same
+    order per tile and the same K-slices, so G is bitwise equal; both within T1 of the oracle."""
+    p = gen.problem(m, n, 1e2, 1e2, 91 + n, with_A=False)
+    Zev = torch.full((n, m + (m & 1)), float("nan"), dtype=torch.float64)
+    Zev[:, :m] = torch.from_numpy(p.Z)
+    Zodd = torch.full((n, m + (1 if m % 2 == 0 else 2)), float("nan"), dtype=torch.float64)
+    Zodd[:, :m] = torch.from_numpy(p.Z)
+    G1 = oqr.gram_euclid(Zev.cuda(), m=m)
+    G2 = oqr.gram_euclid(Zodd.cuda(), m=m)
+    assert torch.equal(G1, G2)
+    G = host(G1).T
+    assert np.array_equal(G, G.T)
+    if m * n <= 2e6:
+        Go = oracle.from_cm(oracle.gram_euclid(p.Z, m), n)
+        Zd = oracle.from_cm(p.Z, m)
+        gate("T1 euclid box |G-G_orc|/M", np.max(np.abs(G - Go) / (np.abs(Zd).T @ np.abs(Zd))), 2 * gamma(3 * m),
+             f"m={m} n={n}")
 
 
 def test_timing_hook_per_kernel(oqr):

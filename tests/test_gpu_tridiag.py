@@ -115,7 +115,8 @@ def test_full_size_config_T(oqr, variant):
     gates(oqr, d, e, p, variant, check_orth=(variant != "normal2"))
 
 
-@pytest.mark.parametrize("m,n", [(2000, 30), (1031, 1), (517, 240), (96, 96), (16, 8), (17, 9), (100000, 200)])
+@pytest.mark.parametrize("m,n", [(2000, 30), (1031, 1), (517, 240), (96, 96), (16, 8), (17, 9), (3001, 145),
+                                 (2003, 209), (100000, 200)])
 def test_fused_stencil_gram_bitwise_packed_path(oqr, m, n):
     """K4t (Z read once by tensor TMA, stencil fused, 20-row boxes with halo) against the packed path
     (Zp and W = T Z through HBM, then K4'), which an odd ldz selects: the same W arithmetic and the
@@ -133,9 +134,7 @@ def test_fused_stencil_gram_bitwise_packed_path(oqr, m, n):
     Zodd = Zodd.cuda()
     G1 = oqr.gram_tridiag(dg, eg, Zev)
     G2 = oqr.gram_tridiag(dg, eg, Zodd)
-    NT = (n + 7) // 8
-    if NT < 22 or NT > 25:   # the same K-slices on both paths (K4t runs two CTA parts per slice
-        assert torch.equal(G1, G2)   # from NT = 22, K4' from NT = 26): bitwise
+    assert torch.equal(G1, G2)   # the same K-slices and CTA parts on both paths: bitwise
     Go = oracle.from_cm(oracle.gram_tridiag(d, e, p.Z, m), n)
     Zd = oracle.from_cm(p.Z, m)
     M = np.abs(Zd).T @ absT_times(d, e, Zd)
