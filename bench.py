@@ -20,7 +20,7 @@ cpu_baseline = the CPU oracle (oracle/, as it stands) on a bounded sample: the l
 --impl reference: the oracle itself timed as the reference arm (rank 0 only).
 --sym: the NEXT-N4 symmetric family (block-lower triangle of A; own roofline).
 --tridiag: the NEXT-N3 second workload (tridiagonal A, m = 100000, n = 200; paper normalisation
-           2mn^2; roofline on the tridiagonal Gram K4t).
+           2mn^2; roofline on the step's dominant kernel, K3 or K4t).
 """
 from __future__ import annotations
 
@@ -228,8 +228,8 @@ def reference_arm(args, cfg, rank):
 def bench_tridiag(args):
     """The paper's second workload (fig.perf-tridiag): A = tridiag(e, d, e),
     m = 100000, n = 200 (gen.TRIDIAG_CONFIGS["T"]), flops normalised 2 m n^2.  Roofline on the
-    tridiagonal Gram K4t (G = Z^T (T Z) on DMMA, Z read once with the stencil fused; the dominant
-    kernel of the step), timed live by the hook."""
+    dominant kernel of the step -- the row substitution K3 or the tridiagonal Gram K4t (G = Z^T (T Z)
+    on DMMA, Z read once with the stencil fused) -- timed live by the hook."""
     import torch
     import oracle
     import paper_1401_5171_b200 as oqr
@@ -264,11 +264,24 @@ def bench_tridiag(args):
     _, _, launches = oqr.timing_read()
     oqr.timing_enable(False)
     k4_ms = kern["K4"][0] / max(kern["K4"][1], 1)
+    k3_ms = kern["K3"][0] / max(kern["K3"][1], 1)
     NT = (n + 7) // 8
-    # K4t computes the upper triangle only (G is symmetric): its algorithmic work is the upper
-    # 8 x 8 tiles incl. the diagonal ones, 2 m 64 NT (NT + 1) / 2 flops
+    # The roofline goes on the dominant kernel of the step (the larger mean launch time):
+    #   K4t computes the upper triangle only (G is symmetric): its algorithmic work is the upper
+    #   8 x 8 tiles incl. the diagonal ones, 2 m 64 NT (NT + 1) / 2 flops (Z read once: 8mn bytes);
+    #   K3 (Q = Z R^{-1}, row substitution): m n^2 flops, 16 m n bytes (Z in, Q out) -- tensor-bound
+    #   at n = 200 (m n^2 / P = 108 us > 16 m n / B = 49 us)
     fl_k4 = 2.0 * m * 64 * NT * (NT + 1) / 2
-    achieved = fl_k4 / (k4_ms * 1e-3) / 1e12
+    fl_k3 = 1.0 * m * n * n
+    if k3_ms > k4_ms:
+        dom, dom_ms, dom_fl = "K3", k3_ms, fl_k3
+        dom_name = "trsm (K3): Q = Z R^{-1} row substitution, off-diagonal tiles on DMMA"
+        traffic_file = "k3_tridiag_traffic.json"
+    else:
+        dom, dom_ms, dom_fl = "K4", k4_ms, fl_k4
+        dom_name = "gram_tridiag (K4t, Z read once by TMA, stencil fused): upper triangle of G = Z^T (T Z)"
+        traffic_file = "k4_tridiag_traffic.json"
+    achieved = dom_fl / (dom_ms * 1e-3) / 1e12
     # e2e: d, e, Z in from pinned host memory, Q, R out, every step
     h2d = (d_h.numel() + e_h.numel() + Z_h.numel()) * 8
     d2h = (Q_h.numel() + R_h.numel()) * 8
@@ -298,7 +311,7 @@ def bench_tridiag(args):
                "sample": f"oracle {args.variant}_tridiag on the leading {mc} rows (tridiagonal of size {mc}, "
                          f"n={n}); {dt:.1f} s; OMP threads={threads}"}
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "k4_tridiag_traffic.json")
+    tp = os.path.join(ROOT, "profiles", traffic_file)
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
@@ -312,15 +325,19 @@ def bench_tridiag(args):
         "config": {"workload": f"tridiag T oqr_{args.variant}_tridiag: m={m}, n={n}, kappa_A=1e3, kappa_Z=1e2",
                    "m": m, "n": n, "variant": args.variant, "flops_per_step": fl,
                    "flop_normalisation": "2mn^2 (PAPER.md:960-961)",
-                   "l2": "Z = %.0f MB, packed Z and T Z = %.0f MB > L2; no flush" % (8e-6 * m * n, 128e-6 * m * NT)},
+                   "l2": "Z = %.0f MB, Q = %.0f MB > L2; no flush" % (8e-6 * m * n, 8e-6 * m * n)},
         "roofline": {"bound": "tensor",
-                     "kernel": "gram_tridiag (K4t, Z read once by TMA, stencil fused): upper triangle of G = Z^T (T Z)",
+                     "kernel": dom_name,
                      "achieved": achieved,
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
-                     "traffic": traffic, "algorithmic_flops_per_launch": fl_k4, "mean_launch_ms": k4_ms,
-                     "share_of_step": k4_ms / ms_step, "peak_source": PEAK_SOURCE,
-                     "other_kernels_ms": {"trsm (K3)": kern["K3"][0] / max(kern["K3"][1], 1),
-                                          "potrf (K2)": kern["K2"][0] / max(kern["K2"][1], 1)}},
+                     "traffic": traffic, "algorithmic_flops_per_launch": dom_fl, "mean_launch_ms": dom_ms,
+                     "share_of_step": dom_ms / ms_step, "peak_source": PEAK_SOURCE,
+                     "other_kernels_ms": {k: v for k, v in {
+                         "gram_tridiag (K4t)": k4_ms, "trsm (K3)": k3_ms,
+                         "potrf (K2)": kern["K2"][0] / max(kern["K2"][1], 1)}.items()
+                         if not k.endswith("(%s)" % ("K4t" if dom == "K4" else dom))},
+                     "k4t_frac": fl_k4 / (k4_ms * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
+                     "k3_frac": fl_k3 / (k3_ms * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": args.e2e_steps, "api": f"H2D copies + oqr_{args.variant}_tridiag + D2H copies"},
@@ -363,7 +380,7 @@ def main():
                     help="NEXT-N4 symmetric family: block-lower triangle of A only (own roofline)")
     ap.add_argument("--tridiag", action="store_true",
                     help="NEXT-N3 second workload: A tridiagonal, m = 100000, n = 200 (paper's 2mn^2 "
-                         "normalisation, own roofline on the tridiagonal Gram K4t)")
+                         "normalisation, roofline on the step's dominant kernel)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded code path even at N = 1 (it is the default for N > 1)")
     args = ap.parse_args()
