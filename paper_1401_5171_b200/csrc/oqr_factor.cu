@@ -25,6 +25,21 @@ __device__ __forceinline__ void dmma_c(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+#ifdef OQR_EXP_POTRF_TRACE  // experiment build only: per-step clock64 stamps of K2's phases
+__device__ long long oqr_k2_trace[4 * 64];
+extern "C" int oqr_exp_k2_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, oqr_k2_trace, sizeof(oqr_k2_trace)) == cudaSuccess ? 0 : -1;
+}
+#define K2_STAMP(i)                                                      \
+  do {                                                                   \
+    if ((i) < 4 * 64) oqr_k2_trace[(i)] = clock64();                     \
+  } while (0)
+#else
+#define K2_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(1024, 1)
 potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ R, int64_t ldr,
              int* info, int info_off, bool first, double* __restrict__ img) {
@@ -56,6 +71,7 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
   }
   if (tid == 0) s_brk = 0;
   __syncthreads();
+  if (tid == 0) K2_STAMP(0);
   __shared__ double s_inv[2][8];  // reciprocals of the diagonal blocks' pivots (double-buffered)
   // warp 0: factor diagonal block jb (rows/cols jb*8..+8) in place; row p scaled by 1/r_pp as
   // LAPACK dpotf2 (DSCAL by ONE/AJJ); breakdown (LAPACK rule) recorded in s_brk.
@@ -135,6 +151,7 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
 #endif
     const int j0 = j * 8;
     __syncthreads();  // diagonal block j factored (look-ahead by warp 0)
+    if (tid == 0) K2_STAMP(4 + 3 * j);
     if (s_brk) break;
     const double* inv = s_inv[j & 1];
     // 2. block row j: columns l >= j0 + 8 (one thread each), forward substitution with R_jj^T
@@ -152,6 +169,7 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
       for (int c = 0; c < 8; ++c) S[pk(j0 + c, l)] = x[c];
     }
     __syncthreads();
+    if (tid == 0) K2_STAMP(5 + 3 * j);
     // 3. trailing update on DMMA, tiles (kt, lt), j < kt <= lt < NT.  Look-ahead: warp 0 updates
     //    the next diagonal tile (t = 0) and factors it at once; warps 1.. take the other tiles.
     const int rem = NT - j - 1;
@@ -161,9 +179,16 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
         update_tile(j0, j0 + 8, j0 + 8);
         __syncwarp();
         factor_diag(j + 1);
+        if (lane == 0) K2_STAMP(6 + 3 * j);
       }
-    } else {
-      for (int t = warp; t < ntiles; t += nwarp - 1) {
+    } else if (warp & 3) {
+      // the trailing tiles go to the warps of sub-partitions 1-3 only (warp w runs on sub-partition
+      // w % 4): DMMA and DFMA share the FP64 pipe, and warp 0's pivot chain (the critical path)
+      // would otherwise queue behind its sub-partition's DMMAs (K2 phase trace,
+      // tools/exp/k2_trace.py: a diagonal factor took up to 9.5k clocks under a full trailing
+      // update, 4.2k without; K2 at n = 200: 100.6 -> 96.6 us)
+      const int widx = warp - (warp >> 2) - 1, nwork = nwarp - (nwarp >> 2);
+      for (int t = 1 + widx; t < ntiles; t += nwork) {  // t = 0 (the next diagonal tile): warp 0
         // t = lt*(lt+1)/2 + kt (local indices): closed form with a one-step fix-up
         int lt = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
         if ((lt + 1) * (lt + 2) / 2 <= t) ++lt;
@@ -177,6 +202,7 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
     if (tid == 0) *info = info_off + s_brk;
     return;
   }
+  if (tid == 0) K2_STAMP(1);
   for (int l = warp; l < n; l += nwarp)
     for (int k = lane; k < n; k += 32) R[(int64_t)l * ldr + k] = (k <= l) ? S[pk(k, l)] : 0.0;
   if (img != nullptr) {
@@ -205,6 +231,7 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
     }
   }
   if (tid == 0 && first) *info = 0;
+  if (tid == 0) K2_STAMP(2);
 }
 
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
