@@ -919,22 +919,28 @@ __host__ __device__ constexpr int up_units(int NT) {  // sum over pairs p of (NT
 #ifndef OQR_EXP_UP_WARPS       // experiment builds only: consumer warps aimed at per part
 #define OQR_EXP_UP_WARPS 16
 #endif
+#ifndef OQR_EXP_UP_TRI_WARPS   // experiment builds only: the same for UPK_TRI
+#define OQR_EXP_UP_TRI_WARPS 11
+#endif
 __host__ __device__ constexpr int up_parts(int NT) {
   return (up_units(NT) + OQR_EXP_UP_PART_UNITS - 1) / OQR_EXP_UP_PART_UNITS;
 }
 __host__ __device__ constexpr int up_part_units(int NT) { return (up_units(NT) + up_parts(NT) - 1) / up_parts(NT); }
-// units per warp: about 16 consumer warps per part (4 per SM sub-partition), 2..UP_MAXC units each
-__host__ __device__ constexpr int up_quota(int NT) {
-  return (up_part_units(NT) + OQR_EXP_UP_WARPS - 1) / OQR_EXP_UP_WARPS < 2
+// units per warp: about 16 consumer warps per part (4 per SM sub-partition), 2..UP_MAXC units each;
+// UPK_TRI: about 11 on three sub-partitions, up to 9 units each (its producers own the fourth)
+__host__ __device__ constexpr int up_maxc(int MODE) { return MODE == UPK_TRI ? 9 : UP_MAXC; }
+__host__ __device__ constexpr int up_target(int MODE) { return MODE == UPK_TRI ? OQR_EXP_UP_TRI_WARPS : OQR_EXP_UP_WARPS; }
+__host__ __device__ constexpr int up_quota(int NT, int MODE) {
+  return (up_part_units(NT) + up_target(MODE) - 1) / up_target(MODE) < 2
              ? 2
-             : ((up_part_units(NT) + OQR_EXP_UP_WARPS - 1) / OQR_EXP_UP_WARPS > UP_MAXC
-                    ? UP_MAXC
-                    : (up_part_units(NT) + OQR_EXP_UP_WARPS - 1) / OQR_EXP_UP_WARPS);
+             : ((up_part_units(NT) + up_target(MODE) - 1) / up_target(MODE) > up_maxc(MODE)
+                    ? up_maxc(MODE)
+                    : (up_part_units(NT) + up_target(MODE) - 1) / up_target(MODE));
 }
 // consumer warps per part, at most: the split of build_upper_sched below, counted at compile time
 // (runs of balanced length, a run cut short where it would reach a third pair)
-__host__ __device__ constexpr int up_wcap(int NT) {
-  const int U = up_units(NT), parts = up_parts(NT), q = up_quota(NT);
+__host__ __device__ constexpr int up_wcap(int NT, int MODE) {
+  const int U = up_units(NT), parts = up_parts(NT), q = up_quota(NT, MODE);
   int best = 0;
   for (int part = 0; part < parts; ++part) {
     const int u0 = U * part / parts, u1 = U * (part + 1) / parts, nu = u1 - u0, w = (nu + q - 1) / q;
@@ -957,7 +963,14 @@ __host__ __device__ constexpr int up_wcap(int NT) {
   }
   return best;
 }
-__host__ __device__ constexpr int up_prod(int MODE) { return MODE == UPK_TRI ? 2 : 1; }  // W formers + TMA issuer
+// Warps of a CTA for nwc consumer warps.  UPK_TRI: the warps of sub-partition 0 (warp w runs on
+// sub-partition w % 4) are the producers -- they form W = T Z and issue the TMA -- and the
+// consumers run on sub-partitions 1-3 only: on sm_100a DFMA/DMUL and DMMA share a sub-partition's
+// FP64 pipe, and producers sharing it with consumers were starved by their DMMAs (ncu "math pipe
+// throttle" on the producer's DMUL, consumers waiting for W).  Other modes: warp 0 issues the TMA.
+__host__ __device__ constexpr int up_total_warps(int nwc, int MODE) {
+  return MODE == UPK_TRI ? nwc + (nwc + 2) / 3 : nwc + 1;
+}
 
 // Per CTA part, per consumer warp: pa, la, l1, pb, lb, len -- units t < l1 are (pair pa, column
 // la + t), units l1 <= t < len are (pair pb, column lb + t - l1).
@@ -1014,9 +1027,9 @@ static bool build_upper_sched(int NT, int parts, int q, int wcap, UpperSched* S)
 // registers per thread: warps are spread over the SM's four sub-partitions, each with a quarter
 // of the register file (16384), so ceil(warps / 4) warps share one quarter
 __host__ __device__ constexpr int up_maxreg(int NT, int MODE) {
-  return (512 / ((up_prod(MODE) + up_wcap(NT) + 3) / 4)) / 8 * 8 > 248
+  return (512 / ((up_total_warps(up_wcap(NT, MODE), MODE) + 3) / 4)) / 8 * 8 > 248
              ? 248
-             : (512 / ((up_prod(MODE) + up_wcap(NT) + 3) / 4)) / 8 * 8;
+             : (512 / ((up_total_warps(up_wcap(NT, MODE), MODE) + 3) / 4)) / 8 * 8;
 }
 
 // One consumer warp's whole block loop, for a run of exactly LEN units (PRED: a run of `len` <= LEN
@@ -1037,11 +1050,12 @@ struct UpShared {
   bool same;
 };
 
-// W(b) = T Z for block i of the slice in B-fragment order, by producer warp pw (of two): k-steps pw
-// and pw + 2, its lane the row r = 4 kk + lane%4 of every n-tile (Zt[c * TRB + TRH + r] =
+
+// W(b) = T Z for block i of the slice in B-fragment order, by producer warp pw of npw: k-steps
+// kk = pw, pw + npw, .., its lane the row r = 4 kk + lane%4 of every n-tile (Zt[c * TRB + TRH + r] =
 // Z[16 b + r, c], r = -2 .. 17); the three z of UPB n-tiles are loaded before any W is stored.
 template <int NT>
-__device__ __forceinline__ void up_form_w(const UpShared& S, int i, int pw, int lane) {
+__device__ __forceinline__ void up_form_w(const UpShared& S, int i, int pw, int npw, int lane) {
   constexpr int FB = NT * 4 * FRAG;
   const int s = i % S.stages, j = i % S.nwb;
   mbar_wait(&S.zfull[s], (i / S.stages) & 1);
@@ -1050,8 +1064,7 @@ __device__ __forceinline__ void up_form_w(const UpShared& S, int i, int pw, int 
   double* __restrict__ W = S.wbuf + j * FB;
   const int64_t r0 = (int64_t)(S.b0 + i) * BK;
 #pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    const int kk = pw + 2 * h;
+  for (int kk = pw; kk < BK / 4; kk += npw) {
     const int r = kk * 4 + (lane & 3);
     const int il = i * BK + r;
     const bool in = r0 + r < S.m;
@@ -1166,8 +1179,7 @@ gram_upper_kernel(const __grid_constant__ CUtensorMap zmap, const double* __rest
                   int64_t m, int nblk, double* __restrict__ P, int stages, int nwb,
                   const __grid_constant__ UpperSched sched) {
   constexpr int NP = NT * 8;
-  constexpr int C = up_quota(NT);
-  constexpr int NPR = up_prod(MODE);
+  constexpr int C = up_quota(NT, MODE);
   constexpr int FB = NT * 4 * FRAG;  // doubles per packed block operand (and per W buffer)
   extern __shared__ __align__(1024) unsigned char smem[];
   UpShared S;
@@ -1217,20 +1229,23 @@ gram_upper_kernel(const __grid_constant__ CUtensorMap zmap, const double* __rest
       tma_g2s_2d(dst, &zmap, b * BK - TRH, 0, &S.zfull[s], pol);
     }
   };
+  const int nwarps = blockDim.x >> 5;
+  const int nprod = MODE == UPK_TRI ? (nwarps + 3) / 4 : 1;  // producer warps
+  const int npw = nprod < BK / 4 ? nprod : BK / 4;           // ... that form W (one k-step or more each)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&S.zfull[s], 1);
       mbar_init(&S.zempty[s], S.nwc);
     }
     for (int j = 0; j < nwb; ++j) {
-      mbar_init(&S.wfull[j], NPR);
+      mbar_init(&S.wfull[j], npw);
       mbar_init(&S.wempty[j], S.nwc);
     }
     mbar_fence_init();
     for (int s = 0; s < stages && s < S.nb; ++s) issue(b0 + s, s);
   }
   __syncthreads();
-  if (warp < NPR) {
+  if (MODE == UPK_TRI ? (warp & 3) == 0 : warp == 0) {
     if constexpr (MODE != UPK_TRI) {  // producer: the ring refills (one elected lane)
       if (lane == 0)
         for (int i = stages; i < S.nb; ++i) {
@@ -1238,9 +1253,11 @@ gram_upper_kernel(const __grid_constant__ CUtensorMap zmap, const double* __rest
           mbar_wait(&S.zempty[s], ((i / stages) - 1) & 1);
           issue(b0 + i, s);
         }
-    } else {  // two producer warps form W; warp 0's lane 0 also refills the ring one block behind
+    } else {  // the producers form W; warp 0's lane 0 also refills the ring one block behind
+      const int pw = warp >> 2;
+      if (pw >= npw) return;
       for (int i = 0; i < S.nb; ++i) {
-        up_form_w<NT>(S, i, warp, lane);
+        up_form_w<NT>(S, i, pw, npw, lane);
         if (warp == 0 && lane == 0 && i >= 1 && i - 1 + stages < S.nb) {
           const int ip = i - 1;
           mbar_wait(&S.zempty[ip % stages], (ip / stages) & 1);
@@ -1250,7 +1267,7 @@ gram_upper_kernel(const __grid_constant__ CUtensorMap zmap, const double* __rest
     }
     return;
   }
-  const int cw = warp - NPR;
+  const int cw = MODE == UPK_TRI ? warp - (warp >> 2) - 1 : warp - 1;
   const unsigned char* tw = sched.w[blockIdx.y][cw];
   double* slot = P + (int64_t)slice * NP * NP;
   const int len = tw[5];
@@ -1287,7 +1304,7 @@ static cudaError_t gram_upper_nt(int64_t m, int n, const double* Z, int64_t ldz,
   *done = false;
   constexpr int NCP = up_parts(NT);
   UpperSched sched;
-  if (!build_upper_sched(NT, NCP, up_quota(NT), up_wcap(NT), &sched)) return cudaErrorInvalidConfiguration;
+  if (!build_upper_sched(NT, NCP, up_quota(NT, MODE), up_wcap(NT, MODE), &sched)) return cudaErrorInvalidConfiguration;
   const int64_t nblk = zp_blocks(m);
   int64_t nsl = num_sms() / NCP;
   if (nsl > nblk) nsl = nblk;
@@ -1316,7 +1333,7 @@ static cudaError_t gram_upper_nt(int64_t m, int n, const double* Z, int64_t ldz,
   if (err != cudaSuccess) return err;
   *g_out = (int)nsl;
   timing_begin(s, OQR_TIMING_K4);
-  gram_upper_kernel<NT, MODE><<<dim3((unsigned)nsl, NCP), 32 * (up_prod(MODE) + sched.nwc), bytes, s>>>(
+  gram_upper_kernel<NT, MODE><<<dim3((unsigned)nsl, NCP), 32 * up_total_warps(sched.nwc, MODE), bytes, s>>>(
       tmap, Xp, Yp, d, e, m, (int)nblk, P, stages, nwb, sched);
   note_launch();
   err = cudaGetLastError();
