@@ -65,10 +65,12 @@ typedef struct CUstream_st* oqr_stream_t;
  *   G = Z^T (A Z) (lines 1-2, fused; A streamed once), R = chol(G) (line 3),
  *   Q = Z R^{-1} by row-wise substitution (line 4).
  * Synchronous: enqueues on `stream`, then synchronises `stream` and returns the status.
- * Small problems (m*m*n <= 1.1e10; all synchronous dense variants): from the second call with the
+ * Small problems (m*m*n <= 1.1e10; all synchronous dense variants -- and the synchronous
+ * tridiagonal oqr_normal/normal2/prequr_tridiag with m*n*n <= 2e10): from the second call with the
  * same arguments (sizes, pointers, stream, device) on, the call replays a CUDA graph of its
  * asynchronous form captured once, with its own cached workspace (same kernels, bitwise the same
- * results; at most 8 such graphs per process; oqr_pool_trim releases them).
+ * results; at most 8 such graphs per process; oqr_pool_trim releases them; never while the
+ * timing hook is on).
  */
 int oqr_normal(int64_t m, int64_t n, const double* A, int64_t lda, const double* Z, int64_t ldz,
                double* Q, double* R, oqr_stream_t stream);

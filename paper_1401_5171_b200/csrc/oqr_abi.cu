@@ -477,20 +477,24 @@ static AOp tridiag_op(const double* d, const double* e) {
 // (variant, sizes, pointers, stream, device) is seen, its asynchronous form is captured once into
 // a CUDA graph with its own persistent workspace, status word and stream; that call and every
 // later identical one replays the graph: the same kernels on the same data layout, so the result
-// is bitwise the direct path's.  Only dense calls with m*m*n <= OQR_GRAPH_MAX_MMN (a large call
-// gains nothing), at most OQR_GRAPH_ENTRIES cached graphs per process (least recently used
-// evicted), never while the timing hook is on.  A call whose entry is in use by another thread,
-// or whose capture fails, takes the direct path.
+// is bitwise the direct path's.  Only dense calls with m*m*n <= OQR_GRAPH_MAX_MMN and tridiagonal
+// calls with m*n*n <= OQR_GRAPH_MAX_MNN (a large call gains nothing; the tridiagonal step at
+// m = 1e5, n = 200 is ~0.6 ms of which ~35 us were launch gaps and the status read), at most
+// OQR_GRAPH_ENTRIES cached graphs per process (least recently used evicted), never while the
+// timing hook is on.  A call whose entry is in use by another thread, or whose capture fails,
+// takes the direct path.
 static constexpr double OQR_GRAPH_MAX_MMN = 1.1e10;
+static constexpr double OQR_GRAPH_MAX_MNN = 2.0e10;
 static constexpr int OQR_GRAPH_ENTRIES = 8;
 
 struct GraphKey {
   int which = -1, dev = -1;
   int64_t m = 0, n = 0, lda = 0, ldz = 0;
   const void *A = nullptr, *Z = nullptr, *Q = nullptr, *R = nullptr, *stream = nullptr;
+  const void *d = nullptr, *e = nullptr;  // tridiagonal A (A == nullptr)
   bool operator==(const GraphKey& o) const {
     return which == o.which && dev == o.dev && m == o.m && n == o.n && lda == o.lda && ldz == o.ldz && A == o.A &&
-           Z == o.Z && Q == o.Q && R == o.R && stream == o.stream;
+           Z == o.Z && Q == o.Q && R == o.R && stream == o.stream && d == o.d && e == o.e;
   }
 };
 
@@ -523,12 +527,16 @@ static int run_variant(int which, const AOp& op, int64_t m, int n, const double*
 // Returns 1 and *status when the call was served by a cached graph; 0 to take the direct path.
 static int graph_call(int which, const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q,
                       double* R, cudaStream_t s, int* status) {
-  if (g_timing || (double)m * (double)m * (double)n > OQR_GRAPH_MAX_MMN) return 0;
+  if (g_timing || op.sym) return 0;
+  if (op.tridiag ? (double)m * (double)n * (double)n > OQR_GRAPH_MAX_MNN
+                 : (double)m * (double)m * (double)n > OQR_GRAPH_MAX_MMN)
+    return 0;
   GraphKey key;
   key.which = which;
   if (cudaGetDevice(&key.dev) != cudaSuccess) return 0;
   key.m = m; key.n = n; key.lda = op.lda; key.ldz = ldz;
   key.A = op.A; key.Z = Z; key.Q = Q; key.R = R; key.stream = s;
+  key.d = op.d; key.e = op.e;
   GraphEntry* e = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_graph_mu);
@@ -610,7 +618,8 @@ static int run_variant(int which, const AOp& op, int64_t m, int n, const double*
   }
 }
 
-// The synchronous dense entry points: a cached graph when one applies, else the direct path.
+// The synchronous dense and tridiagonal entry points: a cached graph when one applies, else the
+// direct path.
 static int sync_call(int which, const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* R,
                      cudaStream_t s) {
   int status = 0;
@@ -807,21 +816,21 @@ int oqr_normal_tridiag(int64_t m, int64_t n, const double* d, const double* e, c
                        double* Q, double* R, oqr_stream_t stream) {
   int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
   if (st) return st;
-  return run_normal(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(0, tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_normal2_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
                         double* Q, double* R, oqr_stream_t stream) {
   int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
   if (st) return st;
-  return run_normal2(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(1, tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_prequr_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,
                        double* Q, double* R, oqr_stream_t stream) {
   int st = check_tridiag(m, n, d, e, Z, ldz, Q, R, true);
   if (st) return st;
-  return run_prequr(tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
+  return sync_call(2, tridiag_op(d, e), m, (int)n, Z, ldz, Q, R, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int oqr_gram_tridiag(int64_t m, int64_t n, const double* d, const double* e, const double* Z, int64_t ldz,

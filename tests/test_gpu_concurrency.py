@@ -87,3 +87,31 @@ def test_cached_graph_calls_bitwise_direct(variant):
         assert torch.equal(Qx, outs[0][0]) and torch.equal(Rx, outs[0][1])
     Q2, R2, st = fn(A, Z)                  # fresh outputs: another key
     assert st == 0 and torch.equal(Q2, outs[0][0]) and torch.equal(R2, outs[0][1])
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+def test_cached_graph_calls_bitwise_direct_tridiag(variant):
+    """The tridiagonal family takes the cached graph too (m n^2 small): replays are bitwise the
+    direct call's; a breakdown status comes back through the graph as through the direct path."""
+    import paper_1401_5171_b200 as oqr
+    m, n = 20000, 64
+    d, e = gen.tridiag(m, 1e3)
+    p = gen.problem(m, n, 1e3, 1e2, 96, with_A=False)
+    dg, eg, Z = torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda(), torch.from_numpy(p.Z).cuda()
+    Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    R = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    fn = oqr.VARIANTS_TRIDIAG[variant]
+    outs = []
+    for _ in range(4):                     # direct, capture + replay, replay, replay
+        Q.fill_(float("nan"))
+        R.fill_(float("nan"))
+        _, _, st = fn(dg, eg, Z, Q, R)
+        assert st == 0
+        outs.append((Q.clone(), R.clone()))
+    for Qx, Rx in outs[1:]:
+        assert torch.equal(Qx, outs[0][0]) and torch.equal(Rx, outs[0][1])
+    # same pointers, new contents: a zero column of Z makes the Gram's pivot exactly 0 -- a
+    # breakdown at that column, reported through the replayed graph's status word
+    Z[1].zero_()
+    _, _, st = fn(dg, eg, Z, Q, R)
+    assert st == 2

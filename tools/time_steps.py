@@ -19,6 +19,7 @@ if cfg in gen.TRIDIAG_CONFIGS:
 
     def timed(fn):
         fn()
+        fn()  # a second identical synchronous call is captured into the library's cached graph
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -50,6 +51,7 @@ Z = torch.from_numpy(p.Z).cuda()
 
 def timed(fn):
     fn()
+    fn()  # a second identical synchronous call is captured into the library's cached graph
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
