@@ -39,6 +39,29 @@ extern "C" int oqr_exp_k2_trace(long long* out) {
   do {              \
   } while (0)
 #endif
+#ifdef OQR_EXP_POTRF_TRACE2  // experiment build only: per-(step, warp) stamps of K2's phases
+__device__ long long oqr_k2_trace2[32 * 32 * 4];
+extern "C" int oqr_exp_k2_trace2(long long* out) {
+  return cudaMemcpyFromSymbol(out, oqr_k2_trace2, sizeof(oqr_k2_trace2)) == cudaSuccess ? 0 : -1;
+}
+#define K2W_STAMP(j, k)                                                         \
+  do {                                                                          \
+    if (lane == 0 && (j) < 32) oqr_k2_trace2[((j) * 32 + warp) * 4 + (k)] = clock64(); \
+  } while (0)
+#else
+#define K2W_STAMP(j, k) \
+  do {                  \
+  } while (0)
+#endif
+
+__device__ __forceinline__ double lds_f64_k2(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f64_k2(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 
 __global__ void __launch_bounds__(1024, 1)
 potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ R, int64_t ldr,
@@ -89,6 +112,7 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
     const int ra = lane >> 3, cb = lane & 7;
     double v0 = (cb >= ra) ? S[pk(b0 + ra, b0 + cb)] : 0.0;
     double v1 = (cb >= ra + 4) ? S[pk(b0 + ra + 4, b0 + cb)] : 0.0;
+    double dA = 1.0, dB = 1.0;  // the pivots of this lane's rows ra, ra + 4 (for the deferred sqrt)
     int brk = 0;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -98,18 +122,24 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
         brk = b0 + c + 1;
         break;
       }
-      // r_cc = sqrt(d), correctly rounded (IEEE sqrt, SURVEY s8(a) S2 -- the same pivot as the
-      // oracle's), computed OFF the pivot chain; the row is scaled by 1/sqrt(d) from one rsqrt
-      // (<= 1 ulp; LAPACK dpotf2 scales by ONE/AJJ), which is what the next pivot waits for --
-      // the sqrt and the reciprocal no longer sit on the 8-pivot chain (inside the gamma_{n+1}
-      // of eq:normal:chol).
+      // The row is scaled by 1/sqrt(d) from one rsqrt (<= 1 ulp; LAPACK dpotf2 scales by
+      // ONE/AJJ), which is what the next pivot waits for (inside the gamma_{n+1} of
+      // eq:normal:chol).  r_cc = sqrt(d), correctly rounded (IEEE sqrt, SURVEY
+      // s8(a) S2 -- the same pivot as the oracle's), is needed by no later operation of the
+      // block: it is taken after the loop for all 8 pivots at once (in-order issue would
+      // otherwise hold the chain behind each sqrt's own dependent sequence -- session 3).
       const double inv = rsqrt(d);
-      const double r = sqrt(d);
-      // row c: (c, c) = r, (c, b > c) *= inv
+      // row c: (c, b > c) *= inv; (c, c) keeps d until the deferred sqrt
       if (c < 4) {
-        if (ra == c) v0 = (cb == c) ? r : (cb > c ? v0 * inv : v0);
+        if (ra == c) {
+          v0 = cb > c ? v0 * inv : v0;
+          dA = d;
+        }
       } else {
-        if (ra + 4 == c) v1 = (cb == c) ? r : (cb > c ? v1 * inv : v1);
+        if (ra + 4 == c) {
+          v1 = cb > c ? v1 * inv : v1;
+          dB = d;
+        }
       }
       if (lane == 0) inv_out[c] = inv;
       // trailing: (a, b) -= r_ca r_cb for c < a <= b; r_cx lives in lane c*8 + x (mod 32)
@@ -121,6 +151,8 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
       if (ra > c && cb >= ra) v0 -= ra0 * rb;
       if (ra + 4 > c && cb >= ra + 4) v1 -= ra1 * rb;
     }
+    if (cb == ra) v0 = sqrt(dA);  // r_cc, c = ra
+    if (cb == ra + 4) v1 = sqrt(dB);  // r_cc, c = ra + 4
     if (cb >= ra) S[pk(b0 + ra, b0 + cb)] = v0;
     if (cb >= ra + 4) S[pk(b0 + ra + 4, b0 + cb)] = v1;
     if (brk && lane == 0) s_brk = brk;
@@ -152,6 +184,7 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
     const int j0 = j * 8;
     __syncthreads();  // diagonal block j factored (look-ahead by warp 0)
     if (tid == 0) K2_STAMP(4 + 3 * j);
+    K2W_STAMP(j, 0);
     if (s_brk) break;
     const double* inv = s_inv[j & 1];
     // 2. block row j: columns l >= j0 + 8 (one thread each), forward substitution with R_jj^T
@@ -168,8 +201,10 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
 #pragma unroll
       for (int c = 0; c < 8; ++c) S[pk(j0 + c, l)] = x[c];
     }
+    K2W_STAMP(j, 1);
     __syncthreads();
     if (tid == 0) K2_STAMP(5 + 3 * j);
+    K2W_STAMP(j, 2);
     // 3. trailing update on DMMA, tiles (kt, lt), j < kt <= lt < NT.  Look-ahead: warp 0 updates
     //    the next diagonal tile (t = 0) and factors it at once; warps 1.. take the other tiles.
     const int rem = NT - j - 1;
@@ -187,16 +222,55 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
       // would otherwise queue behind its sub-partition's DMMAs (K2 phase trace,
       // tools/exp/k2_trace.py: a diagonal factor took up to 9.5k clocks under a full trailing
       // update, 4.2k without; K2 at n = 200: 100.6 -> 96.6 us)
+      // Row strips: the trailing tiles in row-major order (tile row kt = 0..rem-1 local, columns
+      // lt = kt..rem-1; tile 0 = the next diagonal tile is warp 0's), one contiguous run per warp,
+      // so a warp loads the A fragments R_{j,kt} once per tile row it touches.  The update is
+      // shared-memory bound: the per-warp phase trace (tools/exp/k2_trace2.py) put the step-0
+      // trailing update at ~11.7k clocks, and the packed-triangle accesses of a tile cost 36
+      // wavefronts (A 10, B 10, C read+write 16; 16 conflict-free) -- 10.8k for its 300 tiles.
+      // The operations per tile are update_tile's (the same two DMMAs from zero, the same
+      // subtractions), on shared-window offsets.
       const int widx = warp - (warp >> 2) - 1, nwork = nwarp - (nwarp >> 2);
-      for (int t = 1 + widx; t < ntiles; t += nwork) {  // t = 0 (the next diagonal tile): warp 0
-        // t = lt*(lt+1)/2 + kt (local indices): closed form with a one-step fix-up
-        int lt = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-        if ((lt + 1) * (lt + 2) / 2 <= t) ++lt;
-        if (lt * (lt + 1) / 2 > t) --lt;
-        const int kt = t - lt * (lt + 1) / 2;
-        update_tile(j0, (j + 1 + kt) * 8, (j + 1 + lt) * 8);
+      const int T1 = ntiles - 1;  // tiles other than the next diagonal one
+      const int t0 = 1 + (widx * T1) / nwork, t1 = 1 + ((widx + 1) * T1) / nwork;
+      if (t0 < t1) {
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(S);
+        const int c8 = lane >> 2, r4 = lane & 3;
+        int kt = 0, rs = 0;  // rs: row-major index of tile (kt, kt)
+        while (t0 >= rs + (rem - kt)) {
+          rs += rem - kt;
+          ++kt;
+        }
+        int lt = kt + (t0 - rs);
+        int ka = (j + 1 + kt) * 8 + c8;  // output row k = A-fragment column
+        uint32_t ta = sb + 4u * (uint32_t)(ka * (ka + 1)) + 8u * (uint32_t)(j0 + r4);
+        double a0 = lds_f64_k2(ta), a1 = lds_f64_k2(ta + 32u);
+        for (int t = t0;;) {
+          const int kb = (j + 1 + lt) * 8 + c8;  // B-fragment column
+          const uint32_t tb = sb + 4u * (uint32_t)(kb * (kb + 1)) + 8u * (uint32_t)(j0 + r4);
+          double acc[2] = {0.0, 0.0};
+          dmma_c(acc, a0, lds_f64_k2(tb));
+          dmma_c(acc, a1, lds_f64_k2(tb + 32u));
+          const int l = (j + 1 + lt) * 8 + 2 * r4;
+          const uint32_t tc = sb + 4u * (uint32_t)(l * (l + 1)) + 8u * (uint32_t)ka;  // (ka, l)
+          if (ka <= l) sts_f64_k2(tc, lds_f64_k2(tc) - acc[0]);
+          if (ka <= l + 1) {
+            const uint32_t tc1 = tc + 8u * (uint32_t)(l + 1);  // (ka, l + 1)
+            sts_f64_k2(tc1, lds_f64_k2(tc1) - acc[1]);
+          }
+          if (++t == t1) break;
+          if (++lt == rem) {  // next tile row
+            ++kt;
+            lt = kt;
+            ka += 8;
+            ta = sb + 4u * (uint32_t)(ka * (ka + 1)) + 8u * (uint32_t)(j0 + r4);
+            a0 = lds_f64_k2(ta);
+            a1 = lds_f64_k2(ta + 32u);
+          }
+        }
       }
     }
+    K2W_STAMP(j, 3);
   }
   if (s_brk) {
     if (tid == 0) *info = info_off + s_brk;
@@ -303,6 +377,19 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   double v;
   asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
+}
+// v[q] for the lane's quad position q (0..3) by three predicated selects: written as a C
+// ternary chain, ptxas turned the choice into divergent branches with a reconvergence barrier
+// (BSSY/BSYNC) around every A-fragment and Q selection of every tile (cuobjdump; ncu
+// "branch_resolving" 10% of K3's stall samples)
+__device__ __forceinline__ double sel4(int q, double v0, double v1, double v2, double v3) {
+  double r;
+  asm("{\n\t.reg .pred p1, p2, p3;\n\t"
+      "setp.eq.s32 p1, %5, 1;\n\tsetp.eq.s32 p2, %5, 2;\n\tsetp.eq.s32 p3, %5, 3;\n\t"
+      "selp.f64 %0, %2, %1, p1;\n\tselp.f64 %0, %3, %0, p2;\n\tselp.f64 %0, %4, %0, p3;\n\t}"
+      : "=&d"(r)
+      : "d"(v0), "d"(v1), "d"(v2), "d"(v3), "r"(q));
+  return r;
 }
 
 // Warps per CTA: as many as the per-tile register accumulators allow without spills (ptxas:
@@ -471,8 +558,8 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
       }
       // the tile's A fragments (row lane/4, cols 4h + lane%4), then the updates of every later
       // tile, the next one first
-      const double a0 = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
-      const double a1 = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
+      const double a0 = sel4(q4, qv[0], qv[1], qv[2], qv[3]);
+      const double a1 = sel4(q4, qv[4], qv[5], qv[6], qv[7]);
 #ifdef OQR_EXP_TRSM_LDS128  // experiment build: both halves' B values in one LDS.128 (h-interleaved Rt)
 #pragma unroll
       for (int j2 = jt + 1; j2 < NT; ++j2) {
@@ -494,7 +581,7 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = jt * 8 + 2 * q4 + e;
-        const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+        const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
         if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
       }
     }
@@ -654,12 +741,12 @@ trsm_pair_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
           for (int c2 = c + 1; c2 < 8; ++c2) tt[c2] = fma(-qv[c], lds_f64(Rd + 8u * ((t * 8 + c) * 8 + c2)), tt[c2]);
         }
-        const double a0 = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
-        const double a1 = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
+        const double a0 = sel4(q4, qv[0], qv[1], qv[2], qv[3]);
+        const double a1 = sel4(q4, qv[4], qv[5], qv[6], qv[7]);
         if (t + 1 < NT) {  // publish the solved 8 x 8 tile, row-major, for the partner
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+            const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
             myslot[(t & 1) * 64 + (lane >> 2) * 8 + 2 * q4 + e] = qe;
           }
           __syncwarp();
@@ -668,7 +755,7 @@ trsm_pair_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = t * 8 + 2 * q4 + e;
-          const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+          const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
           if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
         }
         // ---- bulk: the deferred q_{t-1} (partner's) and then q_t on this warp's tiles > t, in k
@@ -848,8 +935,8 @@ trsm_panel_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alia
 #pragma unroll
             for (int c2 = c + 1; c2 < 8; ++c2) tt[c2] = fma(-qv[c], lds_f64(Rd + 8u * ((jt * 8 + c) * 8 + c2)), tt[c2]);
           }
-          const double a0 = (q4 == 0) ? qv[0] : (q4 == 1) ? qv[1] : (q4 == 2) ? qv[2] : qv[3];
-          const double a1 = (q4 == 0) ? qv[4] : (q4 == 1) ? qv[5] : (q4 == 2) ? qv[6] : qv[7];
+          const double a0 = sel4(q4, qv[0], qv[1], qv[2], qv[3]);
+          const double a1 = sel4(q4, qv[4], qv[5], qv[6], qv[7]);
 #pragma unroll
           for (int j2 = j + 1; j2 < PWC; ++j2)
             if (t0 + j2 < NT)
@@ -861,7 +948,7 @@ trsm_panel_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alia
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int col = jt * 8 + 2 * q4 + e;
-            const double qe = (q4 == 0) ? qv[e] : (q4 == 1) ? qv[2 + e] : (q4 == 2) ? qv[4 + e] : qv[6 + e];
+            const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
             if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
           }
         }
