@@ -98,6 +98,7 @@ struct Workspace {
   double* Rimg = nullptr;  // K3's image of the last K2 factor (trsm_img_doubles), written by K2
   double* H = nullptr;     // Householder QR scratch (K6): hh_scratch_doubles(m, n)
   int* info = nullptr;
+  int* prog = nullptr;     // progress word of the overlapped K2 -> K3 pair (second half of the info slot)
   cudaStream_t s = nullptr;
   static size_t hh_doubles(int64_t m, int n) { return 2 * cdiv((int64_t)hh_scratch_doubles(m, n), 2); }
   static size_t doubles_for(int64_t m, int n, int64_t mr_local) {
@@ -144,6 +145,7 @@ struct Workspace {
     Rimg = R4 + nn + ((nn & 1) ? 1 : 0);  // 16-byte aligned
     H = Rimg + 2 * cdiv((int64_t)trsm_img_doubles((int)cdiv(n, 8)), 2);
     info = user_info ? user_info : reinterpret_cast<int*>(H + hh_doubles(m, n));
+    prog = reinterpret_cast<int*>(H + hh_doubles(m, n)) + 2;
     return 0;
   }
   ~Workspace() {
@@ -243,14 +245,29 @@ static int gram_euclid_into(int64_t m, int n, const double* Z, int64_t ldz, doub
   return 0;
 }
 
+// Rout = chol(ws.G) and Q = Z Rout^{-1}, the two kernels OVERLAPPED (K3 launched as a programmatic
+// dependent of K2 and following its progress word, DESIGN.md s7 session 4) unless the timing hook
+// is on (its events would serialise them) or the image has no diagonal tiles (n > 232).  The
+// results are bitwise those of the two kernels run one after the other.
+static cudaError_t potrf_trsm(int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* Rout,
+                              int info_off, bool first, Workspace& ws, cudaStream_t s) {
+#ifdef OQR_EXP_NO_OVERLAP  // experiment build only (A/B timing)
+  int* prog = nullptr;
+#else
+  int* prog = (!g_timing && trsm_overlap_ok(n)) ? ws.prog : nullptr;
+#endif
+  cudaError_t e = launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s, first, ws.Rimg, prog);
+  if (e != cudaSuccess) return e;
+  return launch_trsm(m, n, Z, ldz, Rout, n, Q, m, ws.info, s, ws.Rimg, prog);
+}
+
 // One CHOLQR pass: G = Z^T A Z; Rout = chol(G) (info = info_off + k on breakdown);
 // Q = Z Rout^{-1} (Z may be Q itself when ldz == m).
 static int cholqr_pass(const AOp& op, int64_t m, int n, const double* Z, int64_t ldz, double* Q, double* Rout,
                        int info_off, Workspace& ws, cudaStream_t s) {
   int st = gram_into(op, m, n, Z, ldz, ws.G, ws, s);
   if (st) return st;
-  OQR_TRY(launch_potrf(n, ws.G, n, Rout, n, ws.info, info_off, s, info_off == 0, ws.Rimg));
-  OQR_TRY(launch_trsm(m, n, Z, ldz, Rout, n, Q, m, ws.info, s, ws.Rimg));
+  OQR_TRY(potrf_trsm(m, n, Z, ldz, Q, Rout, info_off, info_off == 0, ws, s));
   return 0;
 }
 
@@ -300,8 +317,7 @@ static int run_prequr(const AOp& op, int64_t m, int n, const double* Z, int64_t 
   if (st) return st;
   // pre-step: S = chol(Z^T Z), Y = Z S^{-1} (into Q)
   if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
-  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true, ws.Rimg)))) return st;
-  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s, ws.Rimg)))) return st;
+  if ((st = cuda_status(potrf_trsm(m, n, Z, ldz, Q, ws.R1, 0, true, ws, s)))) return st;
   // A-stage: [Q, U] = CHOLQR(A, Y) in place; breakdown code n + k
   if ((st = cholqr_pass(op, m, n, Q, m, Q, ws.R2, n, ws, s))) return st;
   // R = U S
@@ -376,8 +392,7 @@ static int run_normal_host(int64_t m, int n, const double* A, int64_t lda, const
     if (j == 0) g0 = g;
   }
   if (e == cudaSuccess) e = launch_gram_reduce(n, g0, ws.P, ws.G, n, s, false);
-  if (e == cudaSuccess) e = launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true, ws.Rimg);
-  if (e == cudaSuccess) e = launch_trsm(m, n, Zd, m, ws.R1, n, Qd, m, ws.info, s, ws.Rimg);
+  if (e == cudaSuccess) e = potrf_trsm(m, n, Zd, m, Qd, ws.R1, 0, true, ws, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(Q, Qd, (size_t)m * (size_t)n * 8, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(R, ws.R1, (size_t)n * (size_t)n * 8, cudaMemcpyDeviceToHost, s);
@@ -408,13 +423,11 @@ static int run_prequr_stable(const AOp& op, int64_t m, int n, const double* Z, i
   const double factor = 11.0 * ((double)m * (double)n + (double)n * (double)(n + 1)) * 0x1.0p-53;
   if ((st = gram_euclid_into(m, n, Z, ldz, ws.G, ws, s))) return st;
   if ((st = cuda_status(launch_shift_diag(n, ws.G, n, factor, nullptr, s)))) return st;
-  if ((st = cuda_status(launch_potrf(n, ws.G, n, ws.R1, n, ws.info, 0, s, true, ws.Rimg)))) return st;
-  if ((st = cuda_status(launch_trsm(m, n, Z, ldz, ws.R1, n, Q, m, ws.info, s, ws.Rimg)))) return st;
+  if ((st = cuda_status(potrf_trsm(m, n, Z, ldz, Q, ws.R1, 0, true, ws, s)))) return st;
   double* Rk[2] = {ws.R2, ws.R3};
   for (int pass = 0; pass < 2; ++pass) {  // CholeskyQR2 on Q1, in place
     if ((st = gram_euclid_into(m, n, Q, m, ws.G, ws, s))) return st;
-    if ((st = cuda_status(launch_potrf(n, ws.G, n, Rk[pass], n, ws.info, 0, s, false, ws.Rimg)))) return st;
-    if ((st = cuda_status(launch_trsm(m, n, Q, m, Rk[pass], n, Q, m, ws.info, s, ws.Rimg)))) return st;
+    if ((st = cuda_status(potrf_trsm(m, n, Q, m, Q, Rk[pass], 0, false, ws, s)))) return st;
   }
   if ((st = cuda_status(launch_trmm(n, ws.R3, ws.R2, ws.R4, ws.info, s)))) return st;  // R3 R2
   if ((st = cuda_status(launch_trmm(n, ws.R4, ws.R1, ws.R3, ws.info, s)))) return st;  // S = (R3 R2) R1

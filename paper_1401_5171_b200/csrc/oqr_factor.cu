@@ -63,14 +63,52 @@ __device__ __forceinline__ void sts_f64_k2(uint32_t a, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
+// K3's image of R keeps the strictly upper 8 x 8 tiles (kt, jt), kt < jt, in BLOCK-ROW-major order:
+// tile index trsm_tix = kt (2 NT - kt - 1) / 2 + (jt - kt - 1), so the NT - 1 - kt tiles of block
+// row kt -- what the right-looking solve needs once tile kt is solved, and what K2 finalises in
+// its step kt -- are contiguous (one bulk copy per block row in the overlapped K2 -> K3 pair).
+__host__ __device__ constexpr int trsm_tix(int NT, int kt, int jt) { return kt * (2 * NT - kt - 1) / 2 + (jt - kt - 1); }
+__device__ __forceinline__ void trsm_tile_of(int NT, int t, int* kt_out, int* jt_out) {
+  const float b = (float)(2 * NT - 1);
+  int kt = (int)((b - sqrtf(fmaxf(b * b - 8.0f * (float)t, 0.0f))) * 0.5f);
+  if (kt < 0) kt = 0;
+  if (kt > NT - 2) kt = NT - 2;
+  while (kt > 0 && trsm_tix(NT, kt, kt + 1) > t) --kt;
+  while (kt < NT - 2 && trsm_tix(NT, kt + 1, kt + 2) <= t) ++kt;
+  *kt_out = kt;
+  *jt_out = t - trsm_tix(NT, kt, kt + 1) + kt + 1;
+}
+
+// progress word of the overlapped K2 -> K3 pair (gpu-scope release / acquire)
+__device__ __forceinline__ void prog_store(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int prog_load(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __global__ void __launch_bounds__(1024, 1)
 potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ R, int64_t ldr,
-             int* info, int info_off, bool first, double* __restrict__ img) {
+             int* info, int info_off, bool first, double* __restrict__ img, int* prog) {
   extern __shared__ double S[];
   __shared__ int s_brk;
-  if (!first && *info != 0) return;  // an earlier stage already broke down: keep its code
   const int NT = (n + 7) / 8, NP = NT * 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  // prog != nullptr: K3 runs CONCURRENTLY (launched as a programmatic dependent, session 4): this
+  // kernel publishes K3's image of R block row by block row and raises *prog to the number of
+  // complete block rows (release); -1 tells K3 to do nothing (breakdown, here or earlier).
+  const bool skip = !first && *info != 0;  // an earlier stage already broke down: keep its code
+  if (prog != nullptr) {
+    if (tid == 0) {
+      prog_store(prog, skip ? -1 : 0);
+      __threadfence();
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+  if (skip) return;
   {  // packed upper triangle of G, padded with an identity block; 8 loads in flight per thread
     const int tot = NP * (NP + 1) / 2;
     for (int e0 = tid; e0 < tot; e0 += 8 * 1024) {
@@ -216,6 +254,29 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
         factor_diag(j + 1);
         if (lane == 0) K2_STAMP(6 + 3 * j);
       }
+    } else if (warp == 4 && prog != nullptr) {
+      // Block row j of R and diagonal block j are final: publish their part of K3's image (the
+      // same values as the end-of-kernel image below) and raise the progress word.  Warp 4 idles
+      // in this phase anyway (sub-partition 0 is kept free of DMMAs for warp 0's pivot chain).
+      const int ntri = NT * (NT - 1) / 2 * 64;
+      for (int jt = j + 1; jt < NT; ++jt) {
+        double* dst = img + (size_t)trsm_tix(NT, j, jt) * 64;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          dst[h * 32 + lane] = S[pk(j0 + 4 * h + (lane & 3), jt * 8 + (lane >> 2))];
+      }
+      if (lane < 8) img[ntri + j0 + lane] = (j0 + lane < n) ? 1.0 / S[pk(j0 + lane, j0 + lane)] : 1.0;
+      if (trsm_img_has_rd(NT)) {
+        double* Rd = img + ntri + NT * 8 + j * 64;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = h * 32 + lane, c = e >> 3, c2 = e & 7;
+          Rd[e] = c <= c2 ? S[pk(j0 + c, j0 + c2)] : 0.0;
+        }
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) prog_store(prog, j + 1);
     } else if (warp & 3) {
       // the trailing tiles go to the warps of sub-partitions 1-3 only (warp w runs on sub-partition
       // w % 4): DMMA and DFMA share the FP64 pipe, and warp 0's pivot chain (the critical path)
@@ -273,23 +334,24 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
     K2W_STAMP(j, 3);
   }
   if (s_brk) {
-    if (tid == 0) *info = info_off + s_brk;
+    if (tid == 0) {
+      *info = info_off + s_brk;
+      if (prog != nullptr) prog_store(prog, -1);
+    }
     return;
   }
   if (tid == 0) K2_STAMP(1);
   for (int l = warp; l < n; l += nwarp)
     for (int k = lane; k < n; k += 32) R[(int64_t)l * ldr + k] = (k <= l) ? S[pk(k, l)] : 0.0;
-  if (img != nullptr) {
+  if (img != nullptr && prog == nullptr) {
     // K3's shared-memory image of R (trsm_img_*): the same values K3's prologue would stage from
     // R -- off-diagonal tiles in B-fragment order, the reciprocals of the diagonal, the diagonal
     // tiles -- written once here, so that every K3 CTA lands it with one bulk copy
     const int ntri = NT * (NT - 1) / 2 * 64;
     for (int e = tid; e < ntri; e += blockDim.x) {
-      const int t = e >> 6;
-      int jt = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)t)) * 0.5f);
-      while (jt * (jt - 1) / 2 > t) --jt;
-      while ((jt + 1) * jt / 2 <= t) ++jt;
-      const int kt = t - jt * (jt - 1) / 2, ln = e & 31, h = (e >> 5) & 1;
+      int kt, jt;
+      trsm_tile_of(NT, e >> 6, &kt, &jt);
+      const int ln = e & 31, h = (e >> 5) & 1;
       const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
       img[e] = col < n ? S[pk(k, col)] : 0.0;
     }
@@ -309,13 +371,13 @@ potrf_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restric
 }
 
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
-                         int info_off, cudaStream_t s, bool first, double* img) {
+                         int info_off, cudaStream_t s, bool first, double* img, int* prog) {
   const int NP = 8 * ((n + 7) / 8);
   const size_t bytes = (size_t)NP * (NP + 1) / 2 * sizeof(double);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(potrf_kernel), SMEM_MAX - 1024);
   if (e != cudaSuccess) return e;
   timing_begin(s, OQR_TIMING_K2);
-  potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off, first, img);
+  potrf_kernel<<<1, 1024, bytes, s>>>(n, G, ldg, R, ldr, info, info_off, first, img, prog);
   note_launch();
   e = cudaGetLastError();
   timing_end(s);
@@ -363,7 +425,8 @@ __device__ __forceinline__ void dmma_f(double (&d)[2], double a, double b) {
 }
 
 // R is staged once per (persistent) CTA in shared memory in DMMA B-fragment order:
-//   Rt[((jt*(jt-1)/2 + kt)*2 + h)*32 + lane] = R[kt*8 + 4h + lane%4, jt*8 + lane/4]   (kt < jt)
+//   Rt[(trsm_tix(NT, kt, jt)*2 + h)*32 + lane] = R[kt*8 + 4h + lane%4, jt*8 + lane/4]   (kt < jt;
+//   tiles in block-row-major order, trsm_tix above)
 //   Rd[(jt*8 + c)*8 + c2] = R[jt*8 + c, jt*8 + c2]  (diagonal tiles, upper part)
 //   Ri[jt*8 + c] = 1 / R[jt*8 + c, jt*8 + c]       (1 beyond n)
 // so every fragment load is 256 consecutive bytes.  At NT = 30 Rd does not fit as well (238 KB):
@@ -392,12 +455,81 @@ __device__ __forceinline__ double sel4(int q, double v0, double v1, double v2, d
   return r;
 }
 
+// Overlapped K2 -> K3 (session 4): before tile jt of a warp's first row block.  Warp 0 polls K2's
+// progress word and issues the bulk copies of every newly complete block row c of the image (its
+// NT - 1 - c off-diagonal tiles, contiguous; its 8 reciprocals; its diagonal tile) onto colbar[c];
+// then every warp waits for colbar[jt]: solving tile jt and applying q_jt to the later tiles needs
+// exactly block row jt.  Returns the new `issued`, or -1 when the solve
+// must be abandoned (K2 broke down or was skipped: *prog < 0; or -- a safety net, never seen -- no
+// progress for ~2 s).
+__device__ __forceinline__ int trsm_follow(const int* prog, const double* img, double* rsm, uint64_t* colbar,
+                                           int* s_abort, int NT, int jt, int warp, int lane, int issued) {
+  if (warp == 0 && issued <= jt) {
+    int v = 0;
+    if (lane == 0) {
+      const long long t0 = clock64();
+      for (;;) {
+        v = prog_load(prog);
+        if (v < 0 || v > jt) break;
+        if (clock64() - t0 > 4000000000LL) {
+          v = -1;
+          break;
+        }
+        __nanosleep(64);
+      }
+      if (v < 0) {
+        *reinterpret_cast<volatile int*>(s_abort) = 1;
+      } else {
+        asm volatile("fence.proxy.async;" ::: "memory");  // K2's generic-proxy writes before the async-proxy reads
+        const size_t ntri = (size_t)NT * (NT - 1) / 2 * 64;
+        for (int c = issued; c < v; ++c) {
+          const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&colbar[c]);
+          const uint32_t rowb = (uint32_t)(NT - 1 - c) * 512u;  // block row c: its NT - 1 - c off-diagonal tiles
+          const uint32_t bytes = rowb + 64u + 512u;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+          const size_t o_t = (size_t)trsm_tix(NT, c, c + 1) * 64, o_i = ntri + (size_t)c * 8, o_d = ntri + (size_t)NT * 8 + (size_t)c * 64;
+          if (rowb > 0)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(rsm + o_t)),
+                         "l"(img + o_t), "r"(rowb), "r"(bar)
+                         : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(rsm + o_i)),
+                       "l"(img + o_i), "r"(64u), "r"(bar)
+                       : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(rsm + o_d)),
+                       "l"(img + o_d), "r"(512u), "r"(bar)
+                       : "memory");
+        }
+      }
+    }
+    v = __shfl_sync(0xffffffffu, v, 0);
+    if (v > issued) issued = v;
+  }
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&colbar[jt]);
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar)
+        : "memory");
+    if (ok) return issued;
+    if (*reinterpret_cast<volatile int*>(s_abort)) return -1;
+  }
+}
+
 // Warps per CTA: as many as the per-tile register accumulators allow without spills (ptxas:
 // 16 warps <= 128 registers up to NT = 16, 12 warps <= 168 up to NT = 29, else 8).
 #ifndef OQR_EXP_TRSM_T16
 #define OQR_EXP_TRSM_T16 16
 #endif
+#ifdef OQR_EXP_TRSM_THREADS  // experiment build only (tools/exp/build_k3d.sh)
+__host__ __device__ constexpr int trsm_threads(int) { return OQR_EXP_TRSM_THREADS; }
+#else
 __host__ __device__ constexpr int trsm_threads(int NT) { return NT <= OQR_EXP_TRSM_T16 ? 512 : (NT <= 29 ? 384 : 256); }
+#endif
 
 template <int NT>
 constexpr size_t trsm_smem_doubles(bool with_rd) {
@@ -408,13 +540,28 @@ template <int NT, bool SMEM_RD>
 __global__ void __launch_bounds__(trsm_threads(NT), 1)
 trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias Q (in place)
                  const double* __restrict__ R, int64_t ldr, double* Q, int64_t ldq, const int* info,
-                 const double* __restrict__ img) {
-  if (info != nullptr && *info != 0) return;
+                 const double* __restrict__ img, const int* prog) {
+  // prog != nullptr (SMEM_RD only): this grid runs concurrently with the K2 that produces R
+  // (programmatic dependent launch, session 4).  K2 raises *prog to the number of complete block
+  // rows of the image (-1: breakdown, do nothing); warp 0 lands each new block row's part of the
+  // image with bulk copies on that row's mbarrier, and every warp waits for block row jt's
+  // barrier before tile jt.  info is not consulted in that mode (K2 writes it at its end).
+  if (prog == nullptr && info != nullptr && *info != 0) return;
   extern __shared__ __align__(16) double rsm[];
   double* const Rt_base = rsm;
   double* const Ri_base = rsm + (size_t)NT * (NT - 1) / 2 * 64;
   double* const Rd_base = Ri_base + (size_t)NT * 8;
-  if (img != nullptr) {
+  __shared__ __align__(8) uint64_t colbar[NT];
+  __shared__ int s_abort;
+  if (prog != nullptr) {
+    if (threadIdx.x == 0) {
+      s_abort = 0;
+      for (int c = 0; c < NT; ++c)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&colbar[c])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  } else if (img != nullptr) {
     // K2 wrote this CTA's shared-memory image of R: one bulk copy (SASS UBLKCP) instead of
     // ~20k scattered L2 loads per CTA (the staging loop below: ~10% of K3 at c3)
     __shared__ __align__(8) uint64_t bar;
@@ -453,14 +600,12 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
         const int e = e0 + u * trsm_threads(NT);
         v[u] = 0.0;
         if (e < TOT) {
-          const int t = e >> 6;  // packed triangle tile index: t = jt (jt - 1) / 2 + kt
-          int jt = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)t)) * 0.5f);
-          while (jt * (jt - 1) / 2 > t) --jt;
-          while ((jt + 1) * jt / 2 <= t) ++jt;
+          int kt, jt;  // tile e / 64 of the block-row-major order (trsm_tix)
+          trsm_tile_of(NT, e >> 6, &kt, &jt);
 #ifdef OQR_EXP_TRSM_LDS128
-          const int kt = t - jt * (jt - 1) / 2, ln = (e >> 1) & 31, h = e & 1;
+          const int ln = (e >> 1) & 31, h = e & 1;
 #else
-          const int kt = t - jt * (jt - 1) / 2, ln = e & 31, h = (e >> 5) & 1;
+          const int ln = e & 31, h = (e >> 5) & 1;
 #endif
           const int k = kt * 8 + 4 * h + (ln & 3), col = jt * 8 + (ln >> 2);
           if (col < n) v[u] = R[(int64_t)col * ldr + k];
@@ -488,6 +633,8 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int q4 = lane & 3;                // quad position: C columns 2*q4, 2*q4 + 1
   const int gbase = lane & ~3;            // first lane of this row's quad
+  bool follow = prog != nullptr;          // first row block of the overlapped mode: columns arrive
+  int issued = 0;                         // warp 0: image columns whose copies are in flight
 #pragma unroll 1
   for (int64_t r0 = ((int64_t)blockIdx.x * nw + warp) * 8; r0 < m; r0 += (int64_t)gridDim.x * nw * 8) {
     const int64_t row = r0 + (lane >> 2);
@@ -521,7 +668,11 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = d * 8 + 2 * q4 + e;
+#ifdef OQR_EXP_TRSM_NOLDG  // timing-only diagnostic build: no Z loads (wrong Q)
+        zq[d][e] = (double)(col + lane);
+#else
         zq[d][e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+#endif
       }
 #pragma unroll
     for (int jt = 0; jt < NT; ++jt) {
@@ -530,8 +681,41 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = (jt + PD) * 8 + 2 * q4 + e;
+#ifdef OQR_EXP_TRSM_NOLDG
+          zq[jt % PD][e] = (double)(col + lane);
+#else
           zq[jt % PD][e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
+#endif
         }
+      }
+      // L2 prefetch of this warp's Z chunk (8 columns x 64 B) OQR_EXP_TRSM_PF tiles ahead, running on
+      // into its next row block: costs no registers (a register prefetch distance of 3 or 6 tiles was
+      // slower: spills) and takes 2-5% off K3 (session 4: ncu put 22% of K3's stall samples on the
+      // DADD that consumes a tile's Z values, long scoreboard; distance 4-16 and L1/L2 measured equal)
+#ifndef OQR_EXP_TRSM_PF
+#define OQR_EXP_TRSM_PF 8
+#endif
+#if OQR_EXP_TRSM_PF > 0
+      {
+        const int tp = (jt + OQR_EXP_TRSM_PF) % NT;
+        const int64_t rp = (jt + OQR_EXP_TRSM_PF < NT) ? r0 : r0 + (int64_t)gridDim.x * nw * 8;
+        const int colp = tp * 8 + (lane & 7);
+        if (lane < 8 && colp < n_l && rp < m) {
+          const double* ap = Z + (int64_t)colp * ldz_l + rp;
+#ifdef OQR_EXP_TRSM_PFL1
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(ap));
+#else
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(ap));
+#endif
+        }
+      }
+#endif
+      if (SMEM_RD && follow) {
+        issued = trsm_follow(prog, img, rsm, colbar, &s_abort, NT, jt, warp, lane, issued);
+        if (issued < 0) return;
+        // the R loads below are plain (non-volatile) asm: tie their addresses to this point so that
+        // none of tile jt's is scheduled before its column has landed
+        asm volatile("" : "+r"(Rt), "+r"(Rd), "+r"(Ri) : : "memory");
       }
       double t0 = zc0 - S[jt][0];
       double t1 = zc1 - S[jt][1];
@@ -547,7 +731,13 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int dc = jt * 8 + c;
+#if defined(OQR_EXP_TRSM_NOCHAIN) || defined(OQR_EXP_TRSM_FMAONLY)  // timing-only diagnostic builds (wrong Q)
+        qv[c] = tt[c];
+        (void)dc;
+#else
         qv[c] = tt[c] * lds_f64(Ri + 8u * dc);
+#endif
+#ifndef OQR_EXP_TRSM_NOCHAIN
 #pragma unroll
         for (int c2 = c + 1; c2 < 8; ++c2) {
           double rcj;
@@ -555,6 +745,7 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
           else rcj = (jt * 8 + c2) < n_l ? Rg[(int64_t)(jt * 8 + c2) * ldr + dc] : 0.0;
           tt[c2] = fma(-qv[c], rcj, tt[c2]);
         }
+#endif
       }
       // the tile's A fragments (row lane/4, cols 4h + lane%4), then the updates of every later
       // tile, the next one first
@@ -564,27 +755,37 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #pragma unroll
       for (int j2 = jt + 1; j2 < NT; ++j2) {
         double b0, b1;
-        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(b0), "=d"(b1) : "r"(Rt + 16u * ((j2 * (j2 - 1) / 2 + jt) * 32 + lane)));
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(b0), "=d"(b1) : "r"(Rt + 16u * (trsm_tix(NT, jt, j2) * 32 + lane)));
         dmma_f(S[j2], a0, b0);
         dmma_f(S[j2], a1, b1);
       }
 #else
       // all first-half k-steps, then all second-half ones: consecutive DMMAs are independent
+#ifdef OQR_EXP_TRSM_NOBATCH  // timing-only diagnostic build: only the next tile's two DMMAs (wrong Q)
+      const int JEND = (jt + 2 < NT) ? jt + 2 : NT;
+#else
+      const int JEND = NT;
+#endif
 #pragma unroll
-      for (int j2 = jt + 1; j2 < NT; ++j2)
-        dmma_f(S[j2], a0, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + jt) * 64 + lane)));
+      for (int j2 = jt + 1; j2 < JEND; ++j2)
+        dmma_f(S[j2], a0, lds_f64(Rt + 8u * (trsm_tix(NT, jt, j2) * 64 + lane)));
 #pragma unroll
-      for (int j2 = jt + 1; j2 < NT; ++j2)
-        dmma_f(S[j2], a1, lds_f64(Rt + 8u * ((j2 * (j2 - 1) / 2 + jt) * 64 + 32 + lane)));
+      for (int j2 = jt + 1; j2 < JEND; ++j2)
+        dmma_f(S[j2], a1, lds_f64(Rt + 8u * (trsm_tix(NT, jt, j2) * 64 + 32 + lane)));
 #endif
       // this lane's two C entries -> Q
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = jt * 8 + 2 * q4 + e;
         const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
+#ifdef OQR_EXP_TRSM_NOSTG  // timing-only diagnostic build: no Q stores except a never-true one
+        if (row_ok && col < n_l && qe == 1.2345e300) Q[(int64_t)col * ldq_l + row] = qe;
+#else
         if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+#endif
       }
     }
+    follow = false;
   }
 }
 
@@ -756,7 +957,11 @@ trsm_pair_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
         for (int e = 0; e < 2; ++e) {
           const int col = t * 8 + 2 * q4 + e;
           const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
-          if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+  #ifdef OQR_EXP_TRSM_NOSTG  // timing-only diagnostic build: no Q stores except a never-true one
+        if (row_ok && col < n_l && qe == 1.2345e300) Q[(int64_t)col * ldq_l + row] = qe;
+#else
+        if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+#endif
         }
         // ---- bulk: the deferred q_{t-1} (partner's) and then q_t on this warp's tiles > t, in k
         // order (first halves, then second halves, per k: the same order as the one-warp kernel)
@@ -949,7 +1154,11 @@ trsm_panel_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alia
           for (int e = 0; e < 2; ++e) {
             const int col = jt * 8 + 2 * q4 + e;
             const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
-            if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+    #ifdef OQR_EXP_TRSM_NOSTG  // timing-only diagnostic build: no Q stores except a never-true one
+        if (row_ok && col < n_l && qe == 1.2345e300) Q[(int64_t)col * ldq_l + row] = qe;
+#else
+        if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
+#endif
           }
         }
       }
@@ -966,7 +1175,8 @@ static int trsm_num_sms() {
 
 template <int NT>
 static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
-                           double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img) {
+                           double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img,
+                           const int* prog) {
 #ifdef OQR_EXP_TRSM_PANEL  // experiment build only: the column-panel kernel (measured slower)
   if constexpr (NT > KP_PW) {
     constexpr bool smem_rd = true;
@@ -1018,8 +1228,25 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   int64_t g = cdiv(m, (THREADS / 32) * 8);  // 8 rows per warp per pass
   const int sms = trsm_num_sms();
   if (g > sms) g = sms;          // persistent: R is staged once per CTA
+  if (prog != nullptr) {
+    // overlapped with the K2 launched just before on `s` (launch_potrf with the same prog): a
+    // programmatic dependent launch, one SM left to K2 when the two cannot share one
+    if constexpr (!smem_rd) return cudaErrorInvalidValue;
+    if (g >= sms && sms > 1) g = sms - 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, trsm_dmma_kernel<NT, smem_rd>, m, n, Z, ldz, R, ldr, Q, ldq, info, img, prog);
+  }
   timing_begin(s, OQR_TIMING_K3);
-  trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info, img);
+  trsm_dmma_kernel<NT, smem_rd><<<(unsigned)g, THREADS, bytes, s>>>(m, n, Z, ldz, R, ldr, Q, ldq, info, img, nullptr);
   e = cudaGetLastError();
   timing_end(s);
   return e;
@@ -1029,12 +1256,15 @@ static cudaError_t trsm_nt(int64_t m, int n, const double* Z, int64_t ldz, const
   X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
 
+bool trsm_overlap_ok(int n) { return trsm_img_has_rd((int)cdiv(n, 8)); }
+
 cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
-                        double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img) {
+                        double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img,
+                        const int* prog) {
   cudaError_t e;
   switch ((int)cdiv(n, 8)) {
 #define OQR_CASE(NT) \
-  case NT: e = trsm_nt<NT>(m, n, Z, ldz, R, ldr, Q, ldq, info, s, img); break;
+  case NT: e = trsm_nt<NT>(m, n, Z, ldz, R, ldr, Q, ldq, info, s, img, prog); break;
     OQR_TRSM_CASES(OQR_CASE)
 #undef OQR_CASE
     default: return cudaErrorInvalidValue;

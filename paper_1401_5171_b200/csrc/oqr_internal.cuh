@@ -89,7 +89,7 @@ cudaError_t launch_gram_reduce(int n, int g, const double* P, double* G, int64_t
                                bool sym = false,
                                bool mirror = false);
 // K3's shared-memory image of R, in this order: the strictly upper 8x8 tiles in DMMA B-fragment
-// order (NT(NT-1)/2 * 64 doubles), the reciprocals of the diagonal (NT * 8; 1 beyond n), the
+// order, block row by block row (NT(NT-1)/2 * 64 doubles), the reciprocals of the diagonal (NT * 8; 1 beyond n), the
 // diagonal tiles (NT * 64; only when the whole image fits in shared memory, NT <= 29).
 __host__ __device__ constexpr size_t trsm_img_doubles_rd(int NT, bool rd) {
   return (size_t)NT * (NT - 1) / 2 * 64 + (size_t)NT * 8 + (rd ? (size_t)NT * 64 : 0);
@@ -100,14 +100,20 @@ __host__ __device__ constexpr size_t trsm_img_doubles(int NT) { return trsm_img_
 // nothing if *info != 0 already (an earlier stage broke down), else writes info_off + k on breakdown.
 // img != nullptr: also write K3's image of R there (trsm_img_doubles(ceil(n/8)) doubles, 16-byte
 // aligned) for a launch_trsm with the same R.
+// prog != nullptr (needs img): the OVERLAPPED pair -- the launch_trsm that follows on the same
+// stream with the same img and prog starts while this kernel runs and consumes R's image tile
+// column by tile column (*prog = columns complete, -1 = do nothing); trsm_overlap_ok(n) must hold.
 cudaError_t launch_potrf(int n, const double* G, int64_t ldg, double* R, int64_t ldr, int* info,
-                         int info_off, cudaStream_t s, bool first = true, double* img = nullptr);
+                         int info_off, cudaStream_t s, bool first = true, double* img = nullptr,
+                         int* prog = nullptr);
+bool trsm_overlap_ok(int n);
 // G += factor * tr(G) * I (skipped when *info != 0).
 cudaError_t launch_shift_diag(int n, double* G, int64_t ldg, double factor, const int* info, cudaStream_t s);
 // Q = Z R^{-1}; skipped when info != nullptr && *info != 0.  img: the image launch_potrf wrote for
 // this R (each CTA lands it with one bulk copy), or nullptr (each CTA stages it from R).
 cudaError_t launch_trsm(int64_t m, int n, const double* Z, int64_t ldz, const double* R, int64_t ldr,
-                        double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img = nullptr);
+                        double* Q, int64_t ldq, const int* info, cudaStream_t s, const double* img = nullptr,
+                        const int* prog = nullptr);
 // R = R2 * R1 (upper x upper); skipped when *info != 0.
 cudaError_t launch_trmm(int n, const double* R2, const double* R1, double* R, const int* info,
                         cudaStream_t s);

@@ -115,3 +115,65 @@ def test_cached_graph_calls_bitwise_direct_tridiag(variant):
     Z[1].zero_()
     _, _, st = fn(dg, eg, Z, Q, R)
     assert st == 2
+
+
+@pytest.mark.parametrize("mn", [(3000, 48), (2500, 200), (1031, 9), (900, 232), (900, 240)])
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr", "prequr_stable", "prequr_hh"])
+def test_overlapped_potrf_trsm_bitwise_serial(variant, mn):
+    """K3 is launched as a programmatic dependent of K2 and follows K2's progress word block row by
+    block row (session 4).  With the timing hook on the library takes the serial pair
+    (K2, then K3 on the finished image): the results must be bitwise the same -- for the direct call
+    and for the graph replays, where the two kernels really run concurrently.  n = 240 has no
+    diagonal tiles in the image and always takes the serial pair."""
+    import paper_1401_5171_b200 as oqr
+    m, n = mn
+    p = gen.problem(m, n, 1e3, 1e2, 97)
+    A, Z = torch.from_numpy(p.A).cuda(), torch.from_numpy(p.Z).cuda()
+    fn = oqr.VARIANTS[variant]
+    oqr.timing_enable(True)
+    try:
+        Qs, Rs, st = fn(A, Z)
+    finally:
+        oqr.timing_enable(False)
+    assert st == 0
+    Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    R = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    for rep in range(4):                   # direct, capture + replay, replay, replay
+        Q.fill_(float("nan"))
+        R.fill_(float("nan"))
+        _, _, st = fn(A, Z, Q, R)
+        assert st == 0
+        assert torch.equal(Q, Qs) and torch.equal(R, Rs), (variant, mn, rep)
+
+
+@pytest.mark.parametrize("variant", ["normal", "normal2", "prequr"])
+def test_overlapped_potrf_trsm_breakdown(variant):
+    """A breakdown inside the overlapped pair: K2 tells K3 to stop through the progress word, the
+    status is the serial pair's, and the next (healthy) call through the same cached graph is
+    bitwise the serial result again."""
+    import paper_1401_5171_b200 as oqr
+    m, n = 3000, 120
+    p = gen.problem(m, n, 1e2, 1e2, 98)
+    A, Z = torch.from_numpy(p.A).cuda(), torch.from_numpy(p.Z).cuda()
+    fn = oqr.VARIANTS[variant]
+    oqr.timing_enable(True)
+    try:
+        Qs, Rs, st = fn(A, Z)
+        assert st == 0
+        Zb = Z.clone()
+        Zb[77].zero_()                     # column 77 of Z is zero: pivot 78 of the first Cholesky is 0
+        _, _, stb = fn(A, Zb, check=False)
+    finally:
+        oqr.timing_enable(False)
+    assert stb == 78
+    Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    R = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    Zw = Z.clone()
+    for rep in range(6):                   # healthy / broken alternate through the same pointers
+        broken = rep % 2 == 1
+        Zw.copy_(Zb if broken else Z)
+        _, _, st = fn(A, Zw, Q, R, check=False)
+        if broken:
+            assert st == 78, (variant, rep, st)
+        else:
+            assert st == 0 and torch.equal(Q, Qs) and torch.equal(R, Rs), (variant, rep)

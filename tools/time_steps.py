@@ -74,6 +74,9 @@ res = {"gram (pack+K1+K1r)": timed(lambda: oqr.gram(A, Z, G)),
        "potrf (K2)": timed(lambda: oqr.potrf(G, R, info)),
        "trsm (K3)": timed(lambda: oqr.trsm(Z, R))}
 res["hhqr (K6)"] = timed(lambda: oqr.hhqr(Z, m=m))
+# the variants as a user calls them: hook off (with it on the library takes neither its cached
+# graphs nor the overlapped K2 -> K3 pair)
+oqr.timing_enable(False)
 for v in ("normal", "normal2", "prequr", "prequr_stable", "prequr_hh"):
     Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
     Rv = torch.empty((n, n), dtype=torch.float64, device="cuda")
