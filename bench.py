@@ -344,7 +344,7 @@ def bench_tridiag(args):
                          "gram_tridiag (K4t)": k4_ms, "trsm (K3)": k3_ms,
                          "potrf (K2)": kern["K2"][0] / max(kern["K2"][1], 1)}.items()
                          if not k.endswith("(%s)" % ("K4t" if dom == "K4" else dom))},
-                     "kernel_times": "second pass of the same steps with the per-kernel event hook (direct path)",
+                     "kernel_times": "second pass of the same steps with the per-kernel event hook (direct path, K2 and K3 one after the other; the timed steps run them overlapped)",
                      "k4t_frac": fl_k4 / (k4_ms * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
                      "k3_frac": fl_k3 / (k3_ms * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS},
         "cpu_baseline": cpu,

@@ -636,7 +636,15 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
   bool follow = prog != nullptr;          // first row block of the overlapped mode: columns arrive
   int issued = 0;                         // warp 0: image columns whose copies are in flight
 #pragma unroll 1
-  for (int64_t r0 = ((int64_t)blockIdx.x * nw + warp) * 8; r0 < m; r0 += (int64_t)gridDim.x * nw * 8) {
+#ifndef OQR_EXP_TRSM_MAP
+#define OQR_EXP_TRSM_MAP 0
+#endif
+  // first 8-row block of this warp: 0 = CTA-major (a CTA's warps take adjacent blocks), 1 = warp-major
+  // (the last, partly filled round spreads over all SMs), 2 = warp-pair-major (same, pairs adjacent)
+  const int64_t first_block = OQR_EXP_TRSM_MAP == 1   ? (int64_t)warp * gridDim.x + blockIdx.x
+                              : OQR_EXP_TRSM_MAP == 2 ? ((int64_t)(warp >> 1) * gridDim.x + blockIdx.x) * 2 + (warp & 1)
+                                                      : (int64_t)blockIdx.x * nw + warp;
+  for (int64_t r0 = first_block * 8; r0 < m; r0 += (int64_t)gridDim.x * nw * 8) {
     const int64_t row = r0 + (lane >> 2);
     const bool row_ok = row < m;
     // opaque per-iteration copies: stop the compiler from hoisting loop-invariant R loads and
