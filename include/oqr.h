@@ -294,7 +294,11 @@ int oqr_sum_partials(int64_t n, int64_t count, const double* P, double* G, oqr_s
 /* ---- Measurement hook: per-launch CUDA-event timing of the fused Gram kernel (K1).
  *      When enabled, every K1 launch is bracketed by events recorded on the caller's stream;
  *      oqr_timing_read returns the accumulated milliseconds and launch count since the last
- *      reset (it synchronises on the recorded events).  Not thread-safe; off by default. */
+ *      reset (it synchronises on the recorded events).  Not thread-safe; off by default.
+ *      While it is on, the factorisations run every kernel one after the other: neither the cached
+ *      CUDA graphs of small calls nor the overlapped Cholesky / solve pair (the solve is otherwise
+ *      launched as a programmatic dependent of the Cholesky and runs concurrently with it) are
+ *      taken; the results are bitwise the same either way. */
 void oqr_timing_enable(int enable);
 void oqr_timing_reset(void);
 int oqr_timing_read(double* gram_ms, int64_t* gram_launches, int64_t* total_launches);

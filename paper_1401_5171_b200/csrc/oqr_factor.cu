@@ -637,10 +637,14 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
   int issued = 0;                         // warp 0: image columns whose copies are in flight
 #pragma unroll 1
 #ifndef OQR_EXP_TRSM_MAP
-#define OQR_EXP_TRSM_MAP 0
+#define OQR_EXP_TRSM_MAP 1
 #endif
-  // first 8-row block of this warp: 0 = CTA-major (a CTA's warps take adjacent blocks), 1 = warp-major
-  // (the last, partly filled round spreads over all SMs), 2 = warp-pair-major (same, pairs adjacent)
+  // First 8-row block of this warp.  1 (default) = warp-major: block w * gridDim + cta, so the last,
+  // partly filled round of the persistent loop spreads one warp per SM over all SMs instead of
+  // filling a few CTAs (a lone warp runs its block ~2x faster than one of twelve sharing an SM):
+  // m = 1e5: n = 200 0.257 -> 0.248 ms, n = 100 0.091 -> 0.086; m = 2e4, n = 100 0.036 -> 0.029
+  // (session 4; bitwise the same Q).  0 = CTA-major (adjacent blocks in one CTA), 2 = warp-pair-major
+  // (as 1 with adjacent pairs, measured equal to 1): experiment builds.
   const int64_t first_block = OQR_EXP_TRSM_MAP == 1   ? (int64_t)warp * gridDim.x + blockIdx.x
                               : OQR_EXP_TRSM_MAP == 2 ? ((int64_t)(warp >> 1) * gridDim.x + blockIdx.x) * 2 + (warp & 1)
                                                       : (int64_t)blockIdx.x * nw + warp;
