@@ -462,51 +462,55 @@ __device__ __forceinline__ double sel4(int q, double v0, double v1, double v2, d
 // exactly block row jt.  Returns the new `issued`, or -1 when the solve
 // must be abandoned (K2 broke down or was skipped: *prog < 0; or -- a safety net, never seen -- no
 // progress for ~2 s).
-__device__ __forceinline__ int trsm_follow(const int* prog, const double* img, double* rsm, uint64_t* colbar,
-                                           int* s_abort, int NT, int jt, int warp, int lane, int issued) {
-  if (warp == 0 && issued <= jt) {
-    int v = 0;
-    if (lane == 0) {
-      const long long t0 = clock64();
-      for (;;) {
-        v = prog_load(prog);
-        if (v < 0 || v > jt) break;
-        if (clock64() - t0 > 4000000000LL) {
-          v = -1;
-          break;
-        }
-        __nanosleep(64);
+__device__ __noinline__ int trsm_follow_issue(const int* prog, const double* img, double* rsm, uint64_t* colbar,
+                                              int* s_abort, int NT, int jt, int lane, int issued) {
+  // warp 0 only (out of line: it runs a handful of times per CTA, and inlined at every tile it
+  // made the unrolled body miss in the instruction cache -- ncu no_inst 4% -> 11%)
+  int v = 0;
+  if (lane == 0) {
+    const long long t0 = clock64();
+    for (;;) {
+      v = prog_load(prog);
+      if (v < 0 || v > jt) break;
+      if (clock64() - t0 > 4000000000LL) {
+        v = -1;
+        break;
       }
-      if (v < 0) {
-        *reinterpret_cast<volatile int*>(s_abort) = 1;
-      } else {
-        asm volatile("fence.proxy.async;" ::: "memory");  // K2's generic-proxy writes before the async-proxy reads
-        const size_t ntri = (size_t)NT * (NT - 1) / 2 * 64;
-        for (int c = issued; c < v; ++c) {
-          const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&colbar[c]);
-          const uint32_t rowb = (uint32_t)(NT - 1 - c) * 512u;  // block row c: its NT - 1 - c off-diagonal tiles
-          const uint32_t bytes = rowb + 64u + 512u;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-          const size_t o_t = (size_t)trsm_tix(NT, c, c + 1) * 64, o_i = ntri + (size_t)c * 8, o_d = ntri + (size_t)NT * 8 + (size_t)c * 64;
-          if (rowb > 0)
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(rsm + o_t)),
-                         "l"(img + o_t), "r"(rowb), "r"(bar)
-                         : "memory");
+      __nanosleep(64);
+    }
+    if (v < 0) {
+      *reinterpret_cast<volatile int*>(s_abort) = 1;
+    } else {
+      asm volatile("fence.proxy.async;" ::: "memory");  // K2's generic-proxy writes before the async-proxy reads
+      const size_t ntri = (size_t)NT * (NT - 1) / 2 * 64;
+      for (int c = issued; c < v; ++c) {
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&colbar[c]);
+        const uint32_t rowb = (uint32_t)(NT - 1 - c) * 512u;  // block row c: its NT - 1 - c off-diagonal tiles
+        const uint32_t bytes = rowb + 64u + 512u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        const size_t o_t = (size_t)trsm_tix(NT, c, c + 1) * 64, o_i = ntri + (size_t)c * 8, o_d = ntri + (size_t)NT * 8 + (size_t)c * 64;
+        if (rowb > 0)
           asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           (uint32_t)__cvta_generic_to_shared(rsm + o_i)),
-                       "l"(img + o_i), "r"(64u), "r"(bar)
+                           (uint32_t)__cvta_generic_to_shared(rsm + o_t)),
+                       "l"(img + o_t), "r"(rowb), "r"(bar)
                        : "memory");
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           (uint32_t)__cvta_generic_to_shared(rsm + o_d)),
-                       "l"(img + o_d), "r"(512u), "r"(bar)
-                       : "memory");
-        }
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(rsm + o_i)),
+                     "l"(img + o_i), "r"(64u), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(rsm + o_d)),
+                     "l"(img + o_d), "r"(512u), "r"(bar)
+                     : "memory");
       }
     }
-    v = __shfl_sync(0xffffffffu, v, 0);
-    if (v > issued) issued = v;
   }
+  v = __shfl_sync(0xffffffffu, v, 0);
+  return v > issued ? v : issued;
+}
+__device__ __forceinline__ int trsm_follow(const int* prog, const double* img, double* rsm, uint64_t* colbar,
+                                           int* s_abort, int NT, int jt, int warp, int lane, int issued) {
+  if (warp == 0 && issued <= jt) issued = trsm_follow_issue(prog, img, rsm, colbar, s_abort, NT, jt, lane, issued);
   const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&colbar[jt]);
   for (;;) {
     uint32_t ok;
