@@ -679,17 +679,37 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #endif
     constexpr int PD = OQR_EXP_TRSM_PD;  // Z prefetch distance in tiles
     double zq[PD][2];
+    // Running pointers instead of col * ld + row per access: a smaller unrolled body (-9% SASS), and
+    // the size of this body is itself a cost (instruction cache): m = 1e5, n = 200 0.225 -> 0.217 ms,
+    // n = 232 0.305 -> 0.287 (session 4; bitwise the same Q).  OQR_EXP_TRSM_NOPTR: the indexed form.
+#if !defined(OQR_EXP_TRSM_NOPTR) && !defined(OQR_EXP_TRSM_PTR)
+#define OQR_EXP_TRSM_PTR 1
+#endif
+#ifndef OQR_EXP_TRSM_PF
+#define OQR_EXP_TRSM_PF 8
+#endif
+#ifdef OQR_EXP_TRSM_PTR
+    const double* zp = Z + (int64_t)(2 * q4) * ldz_l + row;  // (row, column 2 q4) of the tile being loaded
+    double* qp = Q + (int64_t)(2 * q4) * ldq_l + row;        // ... of the tile being stored
+    const int64_t zstep = 8 * ldz_l, qstep = 8 * ldq_l;
+#endif
 #pragma unroll
-    for (int d = 0; d < PD; ++d)
+    for (int d = 0; d < PD; ++d) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = d * 8 + 2 * q4 + e;
 #ifdef OQR_EXP_TRSM_NOLDG  // timing-only diagnostic build: no Z loads (wrong Q)
         zq[d][e] = (double)(col + lane);
+#elif defined(OQR_EXP_TRSM_PTR)
+        zq[d][e] = (row_ok && (d < NT - 1 || col < n_l)) ? zp[e ? ldz_l : 0] : 0.0;
 #else
         zq[d][e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
 #endif
       }
+#ifdef OQR_EXP_TRSM_PTR
+      zp += zstep;
+#endif
+    }
 #pragma unroll
     for (int jt = 0; jt < NT; ++jt) {
       const double zc0 = zq[jt % PD][0], zc1 = zq[jt % PD][1];
@@ -699,18 +719,20 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
           const int col = (jt + PD) * 8 + 2 * q4 + e;
 #ifdef OQR_EXP_TRSM_NOLDG
           zq[jt % PD][e] = (double)(col + lane);
+#elif defined(OQR_EXP_TRSM_PTR)
+          zq[jt % PD][e] = (row_ok && (jt + PD < NT - 1 || col < n_l)) ? zp[e ? ldz_l : 0] : 0.0;
 #else
           zq[jt % PD][e] = (row_ok && col < n_l) ? Z[(int64_t)col * ldz_l + row] : 0.0;
 #endif
         }
+#ifdef OQR_EXP_TRSM_PTR
+        zp += zstep;
+#endif
       }
       // L2 prefetch of this warp's Z chunk (8 columns x 64 B) OQR_EXP_TRSM_PF tiles ahead, running on
       // into its next row block: costs no registers (a register prefetch distance of 3 or 6 tiles was
       // slower: spills) and takes 2-5% off K3 (session 4: ncu put 22% of K3's stall samples on the
       // DADD that consumes a tile's Z values, long scoreboard; distance 4-16 and L1/L2 measured equal)
-#ifndef OQR_EXP_TRSM_PF
-#define OQR_EXP_TRSM_PF 8
-#endif
 #if OQR_EXP_TRSM_PF > 0
       {
         const int tp = (jt + OQR_EXP_TRSM_PF) % NT;
@@ -796,10 +818,15 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
         const double qe = sel4(q4, qv[e], qv[2 + e], qv[4 + e], qv[6 + e]);
 #ifdef OQR_EXP_TRSM_NOSTG  // timing-only diagnostic build: no Q stores except a never-true one
         if (row_ok && col < n_l && qe == 1.2345e300) Q[(int64_t)col * ldq_l + row] = qe;
+#elif defined(OQR_EXP_TRSM_PTR)
+        if (row_ok && (jt < NT - 1 || col < n_l)) qp[e ? ldq_l : 0] = qe;
 #else
         if (row_ok && col < n_l) Q[(int64_t)col * ldq_l + row] = qe;
 #endif
       }
+#ifdef OQR_EXP_TRSM_PTR
+      qp += qstep;
+#endif
     }
     follow = false;
   }
