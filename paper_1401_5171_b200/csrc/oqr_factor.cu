@@ -459,7 +459,7 @@ __device__ __forceinline__ double sel4(int q, double v0, double v1, double v2, d
 // progress word and issues the bulk copies of every newly complete block row c of the image (its
 // NT - 1 - c off-diagonal tiles, contiguous; its 8 reciprocals; its diagonal tile) onto colbar[c];
 // then every warp waits for colbar[jt]: solving tile jt and applying q_jt to the later tiles needs
-// exactly block row jt.  Returns the new `issued`, or -1 when the solve
+// exactly block row jt.  Returns the new `issued`, or NT + 1 when the solve
 // must be abandoned (K2 broke down or was skipped: *prog < 0; or -- a safety net, never seen -- no
 // progress for ~2 s).
 __device__ __noinline__ int trsm_follow_issue(const int* prog, const double* img, double* rsm, uint64_t* colbar,
@@ -520,7 +520,7 @@ __device__ __forceinline__ int trsm_follow(const int* prog, const double* img, d
         : "r"(bar)
         : "memory");
     if (ok) return issued;
-    if (*reinterpret_cast<volatile int*>(s_abort)) return -1;
+    if (*reinterpret_cast<volatile int*>(s_abort)) return NT + 1;
   }
 }
 
@@ -750,7 +750,10 @@ trsm_dmma_kernel(int64_t m, int n, const double* Z, int64_t ldz,  // Z may alias
 #endif
       if (SMEM_RD && follow) {
         issued = trsm_follow(prog, img, rsm, colbar, &s_abort, NT, jt, warp, lane, issued);
-        if (issued < 0) return;
+        // Abandoned (K2 broke down or was skipped): stop following and run on over whatever the
+        // image holds -- Q is unspecified on a nonzero status (include/oqr.h) -- rather than leave:
+        // a CTA must not exit while bulk copies into its shared memory may still be in flight.
+        if (issued > NT) follow = false;
         // the R loads below are plain (non-volatile) asm: tie their addresses to this point so that
         // none of tile jt's is scheduled before its column has landed
         asm volatile("" : "+r"(Rt), "+r"(Rd), "+r"(Ri) : : "memory");
